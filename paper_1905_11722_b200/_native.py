@@ -1,0 +1,312 @@
+"""ctypes binding of ``libremat_b200.so`` (the C-ABI in ``include/remat_b200.h``).
+
+There is no fallback: if the library is missing or no CUDA device is visible,
+every solver entry point raises.  Build it with ``python -c "import
+__graft_entry__ as g; g.build()"`` (or ``make -C paper_1905_11722_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .graph import GraphError, pack_graph
+
+LIB_PATH = Path(__file__).resolve().parent / "libremat_b200.so"
+
+OK, INFEASIBLE = 0, 1
+ERR_VALUE, ERR_LATTICE, ERR_CUDA, ERR_NOMEM, ERR_INTERNAL, ERR_RANGE, ERR_SIM = (
+    -1, -2, -3, -4, -5, -6, -7)
+
+FAMILY_CODE = {"full": 0, "pruned": 1}
+OBJECTIVE_CODE = {"minimize": 0, "maximize": 1}
+
+
+class NativeError(RuntimeError):
+    """A CUDA / device failure inside libremat_b200.so."""
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in
+                ("states_visited", "table_entries", "transitions", "dominated_skipped")]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("k", C.c_int32), ("budget", C.c_int64),
+        ("objective_value", C.c_int64), ("peak_memory", C.c_int64), ("overhead", C.c_int64),
+        ("cached_total", C.c_int64), ("stats", Stats),
+    ]
+
+
+class SimInfo(C.Structure):
+    _fields_ = [
+        ("status", C.c_int32), ("err_code", C.c_int32), ("err_index", C.c_int64),
+        ("err_v", C.c_int32), ("err_w", C.c_int32),
+        ("peak_live_memory", C.c_int64), ("total_forward_cost", C.c_int64),
+        ("recompute_cost", C.c_int64), ("backward_count", C.c_int64),
+    ]
+
+
+class Timings(C.Structure):
+    _fields_ = [
+        ("enumerate_ms", C.c_float), ("precompute_ms", C.c_float), ("relax_ms", C.c_float),
+        ("finish_ms", C.c_float), ("total_ms", C.c_float),
+        ("relax_launches", C.c_int64), ("kernel_launches", C.c_int64),
+        ("comparable_pairs", C.c_int64),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+_P = C.c_void_p
+_I32, _I64 = C.c_int32, C.c_int64
+
+
+def lib():
+    """Load the library (once).  Raises ImportError if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: the CUDA extension must be built "
+                "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+        L = C.CDLL(str(LIB_PATH))
+        L.remat_last_error.restype = C.c_char_p
+        L.remat_kernel_launch_count.restype = C.c_int64
+        sigs = {
+            "remat_abi_version": [],
+            "remat_device_count": [C.POINTER(_I32)],
+            "remat_graph_create": [_I32, _I32, _P, _P, _P, _P, C.POINTER(_P)],
+            "remat_graph_free": [_P],
+            "remat_graph_stream": [_P, C.POINTER(_P)],
+            "remat_family_create": [_P, _I32, _I64, C.POINTER(_P)],
+            "remat_family_size": [_P, C.POINTER(_I64)],
+            "remat_family_masks": [_P, _I64, _I64, _P],
+            "remat_family_free": [_P],
+            "remat_family_timings": [_P, C.POINTER(Timings)],
+            "remat_solve": [_P, _P, _I32, _I32, _P, _P, _P, _P],
+            "remat_min_feasible_budget": [_P, _I32, _I32, C.POINTER(_I64), C.POINTER(PlanInfo),
+                                          _P, _P, _P, C.POINTER(_I64), C.POINTER(_I64)],
+            "remat_evaluate": [_P, _I32, _P, C.POINTER(_I64), _P, C.POINTER(_I64),
+                               C.POINTER(_I64), _P],
+            "remat_simulate": [_P, _I32, _P, _P, _P, _P],
+        }
+        for name, args in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        _lib = L
+        return _lib
+
+
+def exported_symbols() -> list[str]:
+    return [
+        "remat_abi_version", "remat_last_error", "remat_device_count",
+        "remat_kernel_launch_count", "remat_graph_create", "remat_graph_free",
+        "remat_graph_stream", "remat_family_create", "remat_family_size",
+        "remat_family_masks", "remat_family_free", "remat_family_timings", "remat_solve",
+        "remat_min_feasible_budget", "remat_evaluate", "remat_simulate",
+    ]
+
+
+def check(rc: int, cap: int | None = None) -> int:
+    if rc >= 0:
+        return rc
+    msg = (lib().remat_last_error() or b"").decode()
+    if rc == ERR_LATTICE:
+        from .lattice import LatticeTooLargeError
+
+        raise LatticeTooLargeError(cap if cap is not None else -1)
+    if rc == ERR_VALUE:
+        raise ValueError(msg)
+    if rc == ERR_RANGE:
+        raise GraphError(msg)
+    if rc == ERR_NOMEM:
+        raise MemoryError(msg)
+    if rc == ERR_INTERNAL:
+        from .planner import PlannerError
+
+        raise PlannerError(msg)
+    raise NativeError(msg or f"libremat_b200 error {rc}")
+
+
+def device_count() -> int:
+    c = _I32(0)
+    rc = lib().remat_device_count(C.byref(c))
+    if rc < 0:
+        return 0
+    return c.value
+
+
+def kernel_launches() -> int:
+    return int(lib().remat_kernel_launch_count())
+
+
+def _default_device() -> int:
+    env = os.environ.get("REMAT_DEVICE")
+    if env is not None:
+        return int(env)
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:
+        pass
+    return 0
+
+
+class DeviceGraph:
+    """A graph resident on one GPU (owns a ``remat_graph_t``)."""
+
+    def __init__(self, g, device: int | None = None):
+        n, w, preds, succs, tcost, mcost = pack_graph(g)
+        self.graph = g
+        self.n, self.w = n, w
+        self.device = _default_device() if device is None else device
+        h = _P()
+        check(lib().remat_graph_create(self.device, n, preds.ctypes.data, succs.ctypes.data,
+                                       tcost.ctypes.data, mcost.ctypes.data, C.byref(h)))
+        self.handle = h
+
+    def stream(self) -> int:
+        s = _P()
+        check(lib().remat_graph_stream(self.handle, C.byref(s)))
+        return s.value or 0
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().remat_graph_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- evaluation / simulation -------------------------------------------------
+
+    def evaluate(self, chain: list[int]):
+        k = len(chain)
+        buf = np.zeros((max(k, 1), self.w), dtype=np.uint64)
+        for s, m in enumerate(chain):
+            for q in range(self.w):
+                buf[s, q] = (m >> (64 * q)) & 0xFFFFFFFFFFFFFFFF
+        stage = np.zeros(max(k, 1), dtype=np.int64)
+        cached = np.zeros((max(k, 1), self.w), dtype=np.uint64)
+        ovh, peak, ctot = _I64(), _I64(), _I64()
+        check(lib().remat_evaluate(self.handle, k, buf.ctypes.data, C.byref(ovh),
+                                   stage.ctypes.data, C.byref(peak), C.byref(ctot),
+                                   cached.ctypes.data))
+        return ovh.value, [int(x) for x in stage[:k]], peak.value, ctot.value, [
+            words_to_int(cached[s]) for s in range(k)]
+
+    def simulate(self, schedules: list[np.ndarray], want_trace: bool = True):
+        offs = np.zeros(len(schedules) + 1, dtype=np.int64)
+        for s, ops in enumerate(schedules):
+            offs[s + 1] = offs[s] + len(ops)
+        total = int(offs[-1])
+        flat = np.zeros((max(total, 1), 2), dtype=np.int32)
+        for s, ops in enumerate(schedules):
+            if len(ops):
+                flat[offs[s]:offs[s + 1]] = ops
+        infos = (SimInfo * len(schedules))()
+        trace = np.zeros(max(total, 1), dtype=np.int64)
+        check(lib().remat_simulate(self.handle, len(schedules), offs.ctypes.data,
+                                   flat.ctypes.data, C.addressof(infos),
+                                   trace.ctypes.data if want_trace else None))
+        return infos, offs, trace
+
+
+def words_to_int(row) -> int:
+    out = 0
+    for k, x in enumerate(row):
+        out |= int(x) << (64 * k)
+    return out
+
+
+class DeviceFamily:
+    """A lower-set family + per-member precompute resident on the GPU."""
+
+    def __init__(self, dg: DeviceGraph, family: str, cap: int):
+        self.dg = dg
+        self.family = family
+        self.cap = cap
+        h = _P()
+        check(lib().remat_family_create(dg.handle, FAMILY_CODE[family], int(cap), C.byref(h)),
+              cap=cap)
+        self.handle = h
+        sz = _I64()
+        check(lib().remat_family_size(h, C.byref(sz)))
+        self.size = sz.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().remat_family_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def masks(self, start: int = 0, count: int | None = None) -> list[int]:
+        if count is None:
+            count = self.size - start
+        buf = np.zeros((max(count, 1), self.dg.w), dtype=np.uint64)
+        check(lib().remat_family_masks(self.handle, start, count, buf.ctypes.data))
+        return [words_to_int(buf[i]) for i in range(count)]
+
+    def timings(self) -> dict:
+        t = Timings()
+        check(lib().remat_family_timings(self.handle, C.byref(t)))
+        return {k: getattr(t, k) for k, _ in Timings._fields_}
+
+    def _alloc(self, nb: int):
+        rows = self.dg.n + 1
+        return (np.zeros((nb, rows, self.dg.w), dtype=np.uint64),
+                np.zeros((nb, rows, self.dg.w), dtype=np.uint64),
+                np.zeros((nb, rows), dtype=np.int64))
+
+    def solve(self, budgets: list[int], objective: str):
+        """Batched dp over ``budgets``: list of (PlanInfo, chain, cached, stages)."""
+        nb = len(budgets)
+        b = np.asarray([min(int(x), 2**62) for x in budgets], dtype=np.int64)
+        infos = (PlanInfo * nb)()
+        chain, cached, stage = self._alloc(nb)
+        check(lib().remat_solve(self.handle, b.ctypes.data, nb, OBJECTIVE_CODE[objective],
+                                C.addressof(infos), chain.ctypes.data, cached.ctypes.data,
+                                stage.ctypes.data))
+        return [self._unpack(infos[i], chain[i], cached[i], stage[i]) for i in range(nb)]
+
+    def min_feasible_budget(self, objective: str, probes_per_round: int = 8):
+        info = PlanInfo()
+        chain, cached, stage = self._alloc(1)
+        bmin, probes, ptrans = _I64(), _I64(), _I64()
+        check(lib().remat_min_feasible_budget(self.handle, OBJECTIVE_CODE[objective],
+                                              probes_per_round, C.byref(bmin), C.byref(info),
+                                              chain.ctypes.data, cached.ctypes.data,
+                                              stage.ctypes.data, C.byref(probes),
+                                              C.byref(ptrans)))
+        return bmin.value, self._unpack(info, chain[0], cached[0], stage[0]), {
+            "probes": probes.value, "probe_transitions": ptrans.value}
+
+    @staticmethod
+    def _unpack(info, chain, cached, stage):
+        k = info.k if info.status == OK else 0
+        return (info,
+                [words_to_int(chain[s]) for s in range(k)],
+                [words_to_int(cached[s]) for s in range(k)],
+                [int(x) for x in stage[:k]])

@@ -1,0 +1,596 @@
+// family.cu — lower-set families and the per-member precompute (K1, K2, K3).
+//
+// K1 enumerate_full   replaces lattice.py:59-84 (all_lower_sets) + from_masks 44-47
+// K2 closure_family   replaces graph.py:98-107 (closures) + lattice.py:87-93
+// K3 member_terms     replaces planner.py:109-115 (boundary, stage_base) plus the
+//                     per-member prefix terms of the pair constants
+//
+// K1 generates level s+1 from level s with the canonical-parent rule (SURVEY
+// Appendix A.7): from lower set L emit L ∪ {v} iff v ∉ L, preds(v) ⊆ L and v is
+// the largest-index maximal element of L ∪ {v}.  Every lower set is emitted
+// exactly once, so no hash/dedup is needed; each level is then ranked by mask
+// value, which reproduces the reference order (popcount, mask).
+#include <algorithm>
+
+#include "device.cuh"
+
+namespace remat {
+
+template <int W>
+__device__ __forceinline__ u64 pick(const u64 (&a)[W], int q) {
+  u64 r = 0;
+#pragma unroll
+  for (int w = 0; w < W; w++)
+    if (w == q) r = a[w];
+  return r;
+}
+
+template <int W>
+__device__ __forceinline__ bool has_bit(const u64 (&a)[W], int v) {
+  return (pick<W>(a, v >> 6) >> (v & 63)) & 1ull;
+}
+
+// ---------------------------------------------------------------------------
+// K1: full lattice, one level at a time
+// ---------------------------------------------------------------------------
+
+// Returns for lane's node v whether L ∪ {v} is a canonical child of L; on
+// success fills the child's maximal-element set.
+template <int W>
+__device__ __forceinline__ bool canonical_child(const u64 (&L)[W], const u64 (&X)[W], int v,
+                                                const u64* __restrict__ preds, u64 (&cx)[W]) {
+  if (has_bit<W>(L, v)) return false;
+  const u64* pv = preds + (size_t)v * W;
+  u64 missing = 0;
+  u64 p[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    p[w] = __ldg(pv + w);
+    missing |= p[w] & ~L[w];
+  }
+  if (missing) return false;
+  // highest maximal element of L that stays maximal in L ∪ {v}
+  int hb = -1;
+#pragma unroll
+  for (int w = W - 1; w >= 0; w--) {
+    u64 y = X[w] & ~p[w];
+    if (hb < 0 && y) hb = w * 64 + 63 - __clzll((long long)y);
+  }
+  if (v < hb) return false;
+#pragma unroll
+  for (int w = 0; w < W; w++) cx[w] = (X[w] & ~p[w]) | ((w == (v >> 6)) ? (1ull << (v & 63)) : 0ull);
+  return true;
+}
+
+template <int W>
+__global__ void k_enum_count(const u64* __restrict__ rows, const u64* __restrict__ maxr,
+                             long long np, const u64* __restrict__ preds, int n,
+                             long long* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const long long p = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= np) return;
+  u64 L[W], X[W], cx[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    L[w] = rows[p * W + w];
+    X[w] = maxr[p * W + w];
+  }
+  int cnt = 0;
+  for (int v0 = 0; v0 < n; v0 += 32) {
+    int v = v0 + lane;
+    bool ok = v < n && canonical_child<W>(L, X, v, preds, cx);
+    cnt += __popc(__ballot_sync(kFull, ok));
+  }
+  if (lane == 0) counts[p] = cnt;
+}
+
+template <int W>
+__global__ void k_enum_emit(const u64* __restrict__ rows, const u64* __restrict__ maxr,
+                            long long np, const u64* __restrict__ preds, int n,
+                            const long long* __restrict__ offs, u64* __restrict__ out_rows,
+                            u64* __restrict__ out_max) {
+  const int lane = threadIdx.x & 31;
+  const long long p = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (p >= np) return;
+  u64 L[W], X[W], cx[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    L[w] = rows[p * W + w];
+    X[w] = maxr[p * W + w];
+  }
+  long long pos = offs[p];
+  for (int v0 = 0; v0 < n; v0 += 32) {
+    int v = v0 + lane;
+    bool ok = v < n && canonical_child<W>(L, X, v, preds, cx);
+    unsigned bal = __ballot_sync(kFull, ok);
+    if (ok) {
+      long long at = pos + __popc(bal & ((1u << lane) - 1));
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        out_rows[at * W + w] = L[w] | ((w == (v >> 6)) ? (1ull << (v & 63)) : 0ull);
+        out_max[at * W + w] = cx[w];
+      }
+    }
+    pos += __popc(bal);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ bool mask_less(const u64* a, const u64* b) {
+#pragma unroll
+  for (int w = W - 1; w >= 0; w--)
+    if (a[w] != b[w]) return a[w] < b[w];
+  return false;
+}
+
+// Rank-sort one level (all members have equal popcount, all distinct):
+// rank(i) = #{k : mask_k < mask_i}.  Tiles of 256 rows staged in shared memory.
+template <int W>
+__global__ void __launch_bounds__(256) k_rank_level(const u64* __restrict__ rows,
+                                                    const u64* __restrict__ maxr, long long N,
+                                                    u64* __restrict__ out_rows,
+                                                    u64* __restrict__ out_max) {
+  __shared__ u64 tile[256 * W];
+  const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+  u64 me[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) me[w] = i < N ? rows[i * W + w] : 0ull;
+  long long rank = 0;
+  for (long long t0 = 0; t0 < N; t0 += 256) {
+    long long cnt = min(256LL, N - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < cnt * W; e += 256) tile[e] = rows[t0 * W + e];
+    __syncthreads();
+    if (i < N)
+      for (int k = 0; k < cnt; k++) rank += mask_less<W>(tile + k * W, me);
+  }
+  if (i < N) {
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+      out_rows[rank * W + w] = me[w];
+      out_max[rank * W + w] = maxr[i * W + w];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: ancestor-closure family
+// ---------------------------------------------------------------------------
+
+// closure(v) = {v} ∪ ⋃ closure(preds(v)); preds have smaller indices, so one
+// sweep in index order suffices (graph.py:98-107).  One warp, lane q owns word q.
+template <int W>
+__global__ void k_closures(const u64* __restrict__ preds, int n, u64* __restrict__ cand) {
+  extern __shared__ u64 clo[];  // [n][W]
+  const int q = threadIdx.x;
+  for (int v = 0; v < n; v++) {
+    u64 c = (q == (v >> 6)) ? (1ull << (v & 63)) : 0ull;
+    for (int w2 = 0; w2 < W; w2++) {
+      u64 x = preds[(size_t)v * W + w2];
+      while (x) {
+        int u = w2 * 64 + __ffsll((long long)x) - 1;
+        x &= x - 1;
+        if (q < W) c |= clo[u * W + q];
+      }
+    }
+    if (q < W) {
+      clo[v * W + q] = c;
+      cand[(size_t)(v + 2) * W + q] = c;
+    }
+    __syncwarp();
+  }
+  if (q < W) {
+    cand[q] = 0ull;  // ∅
+    int lo = q * 64, cnt = n - lo;
+    cand[W + q] = cnt >= 64 ? ~0ull : (cnt <= 0 ? 0ull : ((1ull << cnt) - 1));  // V
+  }
+}
+
+template <int W>
+__device__ __forceinline__ int popc_row(const u64* a) {
+  int c = 0;
+#pragma unroll
+  for (int w = 0; w < W; w++) c += __popcll(a[w]);
+  return c;
+}
+
+// Deduplicate + order the n+2 candidates by (popcount, mask) (from_masks).
+template <int W>
+__global__ void __launch_bounds__(1024) k_pruned_rank(const u64* __restrict__ cand, int N,
+                                                      u64* __restrict__ out_rows,
+                                                      long long* __restrict__ out_count) {
+  extern __shared__ u64 sm[];
+  u64* rows = sm;                              // [N][W]
+  int* keep = reinterpret_cast<int*>(sm + (size_t)N * W);
+  int* pcs = keep + N;
+  for (int e = threadIdx.x; e < N * W; e += blockDim.x) rows[e] = cand[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += blockDim.x) pcs[e] = popc_row<W>(rows + e * W);
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int dup = 0;
+    for (int k = 0; k < e && !dup; k++) {
+      bool eq = true;
+#pragma unroll
+      for (int w = 0; w < W; w++) eq &= rows[k * W + w] == rows[e * W + w];
+      dup = eq;
+    }
+    keep[e] = !dup;
+  }
+  __syncthreads();
+  int local = 0;
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    if (!keep[e]) continue;
+    local++;
+    long long rank = 0;
+    for (int k = 0; k < N; k++) {
+      if (!keep[k]) continue;
+      bool less = pcs[k] != pcs[e] ? pcs[k] < pcs[e] : mask_less<W>(rows + k * W, rows + e * W);
+      rank += less;
+    }
+#pragma unroll
+    for (int w = 0; w < W; w++) out_rows[rank * W + w] = rows[e * W + w];
+  }
+  if (local) atomicAdd(reinterpret_cast<unsigned long long*>(out_count), (unsigned long long)local);
+}
+
+// ---------------------------------------------------------------------------
+// K3: per-member terms
+// ---------------------------------------------------------------------------
+
+// One warp per member L (AoS row).  Produces ∂L (SoA), M(L), T(L), M(∂L),
+// T(L\∂L) and stage_base = M(δ+(L)\L) + M(δ−(δ+(L)\L)\L)  (planner.py:110-115;
+// restricting δ− to successors outside L is exact for lower sets, reference
+// tests/test_strategy.py:97-107).
+template <int W>
+__global__ void k_member_terms(const u64* __restrict__ rows, long long F, GraphView g,
+                               u64* __restrict__ bound_soa, long long* __restrict__ ML,
+                               long long* __restrict__ TL, long long* __restrict__ Mb,
+                               long long* __restrict__ TLnb, long long* __restrict__ base) {
+  __shared__ u64 bsh[8][W];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (i >= F) return;
+  u64 L[W], dp[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    L[w] = rows[i * W + w];
+    dp[w] = 0;
+  }
+  if (lane < W) bsh[wib][lane] = 0;
+  __syncwarp();
+  long long ml = 0, tl = 0, mb = 0, tlnb = 0;
+  for (int v0 = 0; v0 < g.n; v0 += 32) {
+    int v = v0 + lane;
+    bool isb = false;
+    if (v < g.n && has_bit<W>(L, v)) {
+      const u64* sv = g.succs + (size_t)v * W;
+      u64 outside = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        u64 s = __ldg(sv + w);
+        dp[w] |= s;
+        outside |= s & ~L[w];
+      }
+      long long m = __ldg(g.M + v), t = __ldg(g.T + v);
+      ml += m;
+      tl += t;
+      isb = outside != 0;
+      if (isb) mb += m; else tlnb += t;
+    }
+    unsigned bal = __ballot_sync(kFull, isb);
+    if (lane == 0) bsh[wib][v0 >> 6] |= (u64)bal << (v0 & 63);
+  }
+  ml = warp_sum(ml);
+  tl = warp_sum(tl);
+  mb = warp_sum(mb);
+  tlnb = warp_sum(tlnb);
+  u64 D[W], dm[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    D[w] = warp_or(dp[w]) & ~L[w];
+    dm[w] = 0;
+  }
+  long long md = 0;
+  for (int v0 = 0; v0 < g.n; v0 += 32) {
+    int v = v0 + lane;
+    if (v < g.n && has_bit<W>(D, v)) {
+      md += __ldg(g.M + v);
+      const u64* pv = g.preds + (size_t)v * W;
+#pragma unroll
+      for (int w = 0; w < W; w++) dm[w] |= __ldg(pv + w);
+    }
+  }
+  md = warp_sum(md);
+  u64 E[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) E[w] = warp_or(dm[w]) & ~L[w];
+  long long me = 0;
+  for (int v0 = 0; v0 < g.n; v0 += 32) {
+    int v = v0 + lane;
+    if (v < g.n && has_bit<W>(E, v)) me += __ldg(g.M + v);
+  }
+  me = warp_sum(me);
+  __syncwarp();
+  if (lane < W) bound_soa[(size_t)lane * F + i] = bsh[wib][lane];
+  if (lane == 0) {
+    ML[i] = ml;
+    TL[i] = tl;
+    Mb[i] = mb;
+    TLnb[i] = tlnb;
+    base[i] = md + me;
+  }
+}
+
+template <int W>
+__global__ void k_to_soa(const u64* __restrict__ rows, long long F, u64* __restrict__ soa) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+#pragma unroll
+  for (int w = 0; w < W; w++) soa[(size_t)w * F + i] = rows[i * W + w];
+}
+
+template <int W>
+__global__ void k_popcount_hist(const u64* __restrict__ rows, long long F, long long* hist) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+  atomicAdd(reinterpret_cast<unsigned long long*>(hist + popc_row<W>(rows + i * W)), 1ull);
+}
+
+__global__ void k_row_len(const long long* __restrict__ TL, long long F, long long* out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < F) out[i] = TL[i] + 1;
+}
+
+__global__ void k_level_max(const long long* __restrict__ TL, const long long* __restrict__ ls,
+                            long long* __restrict__ out) {
+  __shared__ long long red[32];
+  const int s = blockIdx.x;
+  long long lo = ls[s], hi = ls[s + 1], mx = 0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) mx = max(mx, TL[i] + 1);
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, m));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); k++) mx = max(mx, red[k]);
+    out[s] = mx;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan (int64)
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(1024) k_scan_block(const long long* __restrict__ in,
+                                                     long long* __restrict__ out, long long n,
+                                                     long long* __restrict__ sums) {
+  __shared__ long long scratch[33];
+  long long i = (long long)blockIdx.x * 1024 + threadIdx.x;
+  long long v = i < n ? in[i] : 0;
+  long long tot;
+  long long ex = block_exclusive_sum(v, scratch, &tot);
+  if (i < n) out[i] = ex;
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void k_scan_add(long long* __restrict__ out, long long n,
+                           const long long* __restrict__ offs) {
+  long long i = (long long)blockIdx.x * 1024 + threadIdx.x;
+  if (i < n) out[i] += offs[blockIdx.x];
+}
+
+static int scan_rec(const long long* in, long long* out, long long n, cudaStream_t s) {
+  long long nb = (n + 1023) / 1024;
+  long long* sums = nullptr;
+  RM_CUDA(cudaMallocAsync(&sums, sizeof(long long) * (nb + 1), s));
+  k_scan_block<<<(unsigned)nb, 1024, 0, s>>>(in, out, n, sums);
+  RM_LAUNCHED();
+  if (nb > 1) {
+    long long* soff = nullptr;
+    RM_CUDA(cudaMallocAsync(&soff, sizeof(long long) * (nb + 1), s));
+    int rc = scan_rec(sums, soff, nb, s);
+    if (rc < 0) return rc;
+    k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(out, n, soff);
+    RM_LAUNCHED();
+    RM_CUDA(cudaFreeAsync(soff, s));
+  }
+  RM_CUDA(cudaFreeAsync(sums, s));
+  return REMAT_OK;
+}
+
+int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_t s,
+                   long long* total_host) {
+  if (n <= 0) {
+    if (total_host) *total_host = 0;
+    return REMAT_OK;
+  }
+  int rc = scan_rec(in, out, n, s);
+  if (rc < 0) return rc;
+  if (total_host) {
+    long long a = 0, b = 0;
+    RM_CUDA(cudaMemcpyAsync(&a, out + n - 1, sizeof a, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaMemcpyAsync(&b, in + n - 1, sizeof b, cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    *total_host = a + b;
+  }
+  return REMAT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host drivers
+// ---------------------------------------------------------------------------
+
+template <int W>
+static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
+                          std::vector<long long>& level_start) {
+  cudaStream_t s = g->stream;
+  const int n = g->n;
+  long long Fcap = std::max<long long>(1024, std::min<long long>(cap, 1 << 16));
+  int rc = fam.ensure((size_t)Fcap * W);
+  if (rc < 0) return rc;
+  DevBuf<u64> maxc, maxn, nrows, nmax;
+  DevBuf<long long> counts, offs;
+  if ((rc = maxc.ensure(W)) < 0) return rc;
+  RM_CUDA(cudaMemsetAsync(fam.p, 0, sizeof(u64) * W, s));
+  RM_CUDA(cudaMemsetAsync(maxc.p, 0, sizeof(u64) * W, s));
+  level_start.assign(1, 0);
+  long long width = 1, F = 1;
+  for (int lvl = 0; lvl < n; lvl++) {
+    const u64* cur = fam.p + (size_t)level_start.back() * W;
+    if ((rc = counts.ensure(width)) < 0 || (rc = offs.ensure(width)) < 0) return rc;
+    unsigned blocks = (unsigned)((width + 7) / 8);
+    k_enum_count<W><<<blocks, 256, 0, s>>>(cur, maxc.p, width, g->preds.p, n, counts.p);
+    RM_LAUNCHED();
+    long long next = 0;
+    if ((rc = scan_exclusive(counts.p, offs.p, width, s, &next)) < 0) return rc;
+    if (F + next > cap)
+      return fail(REMAT_ERR_LATTICE, "lattice too large: more than " + std::to_string(cap) +
+                                         " lower sets; raise the cap or use the pruned family");
+    if ((rc = nrows.ensure((size_t)next * W)) < 0 || (rc = nmax.ensure((size_t)next * W)) < 0)
+      return rc;
+    k_enum_emit<W><<<blocks, 256, 0, s>>>(cur, maxc.p, width, g->preds.p, n, offs.p, nrows.p,
+                                          nmax.p);
+    RM_LAUNCHED();
+    if (F + next > Fcap) {
+      long long nc = Fcap;
+      while (nc < F + next) nc *= 2;
+      u64* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, sizeof(u64) * W * nc);
+      if (e != cudaSuccess) return fail(REMAT_ERR_NOMEM, "family buffer allocation failed");
+      RM_CUDA(cudaMemcpyAsync(p, fam.p, sizeof(u64) * W * F, cudaMemcpyDeviceToDevice, s));
+      RM_CUDA(cudaStreamSynchronize(s));
+      cudaFree(fam.p);
+      fam.p = p;
+      fam.n = (size_t)nc * W;
+      Fcap = nc;
+    }
+    level_start.push_back(F);
+    if ((rc = maxn.ensure((size_t)next * W)) < 0) return rc;
+    k_rank_level<W><<<(unsigned)((next + 255) / 256), 256, 0, s>>>(
+        nrows.p, nmax.p, next, fam.p + (size_t)F * W, maxn.p);
+    RM_LAUNCHED();
+    std::swap(maxc.p, maxn.p);
+    std::swap(maxc.n, maxn.n);
+    F += next;
+    width = next;
+  }
+  level_start.push_back(F);
+  return REMAT_OK;
+}
+
+template <int W>
+static int enumerate_pruned(remat_graph_s* g, DevBuf<u64>& fam, long long* Fout) {
+  cudaStream_t s = g->stream;
+  const int n = g->n, N = n + 2;
+  DevBuf<u64> cand;
+  DevBuf<long long> cnt;
+  int rc;
+  if ((rc = cand.ensure((size_t)N * W)) < 0 || (rc = fam.ensure((size_t)N * W)) < 0 ||
+      (rc = cnt.ensure(1)) < 0)
+    return rc;
+  size_t sm1 = sizeof(u64) * n * W;
+  RM_CUDA(cudaFuncSetAttribute(k_closures<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(sm1, 1)));
+  k_closures<W><<<1, 32, sm1, s>>>(g->preds.p, n, cand.p);
+  RM_LAUNCHED();
+  size_t sm2 = sizeof(u64) * N * W + 2 * sizeof(int) * N;
+  RM_CUDA(cudaFuncSetAttribute(k_pruned_rank<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sm2));
+  RM_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(long long), s));
+  k_pruned_rank<W><<<1, 1024, sm2, s>>>(cand.p, N, fam.p, cnt.p);
+  RM_LAUNCHED();
+  RM_CUDA(cudaMemcpyAsync(Fout, cnt.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  return REMAT_OK;
+}
+
+template <int W>
+static int build_family_w(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
+  cudaStream_t s = g->stream;
+  Events& ev = g->ev;
+  RM_CUDA(cudaEventRecord(ev.e[0], s));
+  DevBuf<u64> aos;
+  int rc;
+  long long F = 0;
+  if (kind == REMAT_FAMILY_FULL) {
+    rc = enumerate_full<W>(g, cap, aos, f->level_start);
+    if (rc < 0) return rc;
+    F = f->level_start.back();
+  } else {
+    rc = enumerate_pruned<W>(g, aos, &F);
+    if (rc < 0) return rc;
+  }
+  f->F = F;
+  RM_CUDA(cudaEventRecord(ev.e[1], s));
+  if ((rc = f->masks.ensure((size_t)F * W)) < 0 || (rc = f->bound.ensure((size_t)F * W)) < 0 ||
+      (rc = f->ML.ensure(F)) < 0 || (rc = f->TL.ensure(F)) < 0 || (rc = f->Mb.ensure(F)) < 0 ||
+      (rc = f->TLnb.ensure(F)) < 0 || (rc = f->base.ensure(F)) < 0 ||
+      (rc = f->foff.ensure(F + 1)) < 0)
+    return rc;
+  k_to_soa<W><<<(unsigned)((F + 255) / 256), 256, 0, s>>>(aos.p, F, f->masks.p);
+  RM_LAUNCHED();
+  k_member_terms<W><<<(unsigned)((F + 7) / 8), 256, 0, s>>>(aos.p, F, g->view(), f->bound.p,
+                                                            f->ML.p, f->TL.p, f->Mb.p,
+                                                            f->TLnb.p, f->base.p);
+  RM_LAUNCHED();
+  const int n = g->n;
+  DevBuf<long long> tmp, lsd, lmax;
+  if ((rc = tmp.ensure(std::max<long long>(F, n + 2))) < 0 || (rc = lsd.ensure(n + 2)) < 0 ||
+      (rc = lmax.ensure(n + 1)) < 0)
+    return rc;
+  if (kind == REMAT_FAMILY_PRUNED) {
+    RM_CUDA(cudaMemsetAsync(tmp.p, 0, sizeof(long long) * (n + 1), s));
+    k_popcount_hist<W><<<(unsigned)((F + 255) / 256), 256, 0, s>>>(aos.p, F, tmp.p);
+    RM_LAUNCHED();
+    std::vector<long long> hist(n + 1);
+    RM_CUDA(cudaMemcpyAsync(hist.data(), tmp.p, sizeof(long long) * (n + 1),
+                            cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    f->level_start.assign(n + 2, 0);
+    for (int l = 0; l <= n; l++) f->level_start[l + 1] = f->level_start[l] + hist[l];
+  }
+  RM_CUDA(cudaMemcpyAsync(lsd.p, f->level_start.data(), sizeof(long long) * (n + 2),
+                          cudaMemcpyHostToDevice, s));
+  k_level_max<<<n + 1, 256, 0, s>>>(f->TL.p, lsd.p, lmax.p);
+  RM_LAUNCHED();
+  k_row_len<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(f->TL.p, F, tmp.p);
+  RM_LAUNCHED();
+  long long slots = 0;
+  if ((rc = scan_exclusive(tmp.p, f->foff.p, F, s, &slots)) < 0) return rc;
+  RM_CUDA(cudaMemcpyAsync(f->foff.p + F, &slots, sizeof(long long), cudaMemcpyHostToDevice, s));
+  f->slots = slots;
+  f->level_maxR.assign(n + 1, 0);
+  RM_CUDA(cudaMemcpyAsync(f->level_maxR.data(), lmax.p, sizeof(long long) * (n + 1),
+                          cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaEventRecord(ev.e[2], s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, ev.e[0], ev.e[1]);
+  cudaEventElapsedTime(&b, ev.e[1], ev.e[2]);
+  f->timings.enumerate_ms = a;
+  f->timings.precompute_ms = b;
+  return REMAT_OK;
+}
+
+int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
+  int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
+  f->g = g;
+  f->kind = kind;
+  dispatch_words(g->Wp, [&](auto wc) {
+    constexpr int W = decltype(wc)::value;
+    rc = build_family_w<W>(g, kind, cap, f);
+  });
+  if (rc < 0) return rc;
+  // packed row keys (m << IB | parent) need M(V) < 2^(64-IB)
+  int ib = 1;
+  while ((1LL << ib) < f->F) ib++;
+  f->IB = ib;
+  if (ib >= 62 || (unsigned long long)g->MV >= ((~0ull) >> ib) - 1)
+    return fail(REMAT_ERR_RANGE, "total memory cost " + std::to_string(g->MV) +
+                                     " too large for packed DP keys with a family of " +
+                                     std::to_string(f->F) + " members");
+  return REMAT_OK;
+}
+
+}  // namespace remat

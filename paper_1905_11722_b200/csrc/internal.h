@@ -1,0 +1,246 @@
+// internal.h — shared host/device declarations of libremat_b200.so.
+//
+// Layout in HBM (see DESIGN.md §Data layout):
+//   graph:   preds/succs [n][Wp] u64 (AoS: a node's set is one 8·Wp-byte row),
+//            T/M int64[n], weight-class masks [K][Wp]
+//   family:  masks/bound SoA [Wp][F] u64 (word w of member i at w*F+i, so a
+//            warp reading 32 consecutive members' word w is one coalesced
+//            256-byte transaction), per-member int64 scalars ML, TL, Mb, TLnb,
+//            base, frontier slot offsets foff[F+1]
+//   DP:      per budget b: Frontier entries (16 B) in slots
+//            [b*slots + foff[j], b*slots + foff[j+1]) — capacity T(L_j)+1, the
+//            dense row length — plus flen/ccount/trans [nb][F].
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/remat_b200.h"
+
+typedef unsigned long long u64;
+
+namespace remat {
+
+constexpr int kMaxWords = 16;        // n <= 1024
+constexpr int kMaxClasses = 32;      // weight classes per cost vector
+constexpr int kRelaxThreads = 256;
+constexpr int kRelaxWarps = kRelaxThreads / 32;
+
+// One non-dominated DP entry (t, m) of a member plus its back-pointer
+// (DpTable.opt / parent, reference planner.py:82-92).  16 bytes -> one LDG.128.
+struct __align__(16) Frontier {
+  long long m;     // cached memory (opt value)
+  unsigned t;      // accumulated overhead
+  int parent;      // family index of the predecessor cell (-1 for ∅)
+};
+
+// Words per set, padded to an instantiated width.
+inline int padded_words(int w) {
+  static const int kW[] = {1, 2, 3, 4, 6, 8, 9, 12, 16};
+  for (int x : kW)
+    if (x >= w) return x;
+  return -1;
+}
+
+template <typename F>
+void dispatch_words(int Wp, F&& f) {
+  switch (Wp) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 3: f(std::integral_constant<int, 3>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 6: f(std::integral_constant<int, 6>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    case 9: f(std::integral_constant<int, 9>{}); break;
+    case 12: f(std::integral_constant<int, 12>{}); break;
+    case 16: f(std::integral_constant<int, 16>{}); break;
+    default: break;
+  }
+}
+
+struct Status {
+  int code = REMAT_OK;
+  std::string msg;
+  bool ok() const { return code >= 0; }
+};
+
+void set_error(int code, const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+#define RM_CUDA(call)                                           \
+  do {                                                          \
+    cudaError_t _e = (call);                                    \
+    if (_e != cudaSuccess) return ::remat::cuda_fail(_e, #call); \
+  } while (0)
+
+#define RM_LAUNCHED()                                               \
+  do {                                                              \
+    ::remat::count_launch();                                        \
+    cudaError_t _e = cudaGetLastError();                            \
+    if (_e != cudaSuccess) return ::remat::cuda_fail(_e, "launch"); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device-side views passed to kernels by value
+// ---------------------------------------------------------------------------
+
+struct GraphView {
+  int n, Wp;
+  const u64* preds;   // [n][Wp]
+  const u64* succs;   // [n][Wp]
+  const long long* T; // [n]
+  const long long* M; // [n]
+};
+
+struct FamilyView {
+  long long F;
+  const u64* masks;  // SoA [Wp][F]
+  const u64* bound;  // SoA [Wp][F]
+  const long long *ML, *TL, *Mb, *TLnb, *base;
+  const long long* foff;  // [F+1]
+};
+
+struct ClassView {
+  int enabled;                    // 0 -> class path unavailable (> kMaxClasses)
+  int KT, KM;
+  const u64* clsT;                // [KT][Wp]
+  const u64* clsM;                // [KM][Wp]
+  const long long* coefT;         // [KT]
+  const long long* coefM;         // [KM]
+};
+
+struct DpView {
+  long long slots;           // frontier slots per budget
+  Frontier* frontier;        // [nb][slots]
+  int* flen;                 // [nb][F]
+  int* ccount;               // [nb][F]
+  long long* trans;          // [nb][F]
+  const long long* budgets;  // [nb] (clamped to 2*M(V))
+  int IB;                    // parent-index bits in packed row keys
+  int maximize;
+};
+
+// ---------------------------------------------------------------------------
+// host handles
+// ---------------------------------------------------------------------------
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  int ensure(size_t count) {
+    if (count <= n && p) return REMAT_OK;
+    release();
+    size_t c = count ? count : 1;
+    cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(REMAT_ERR_NOMEM, "device allocation of " + std::to_string(c * sizeof(T)) +
+                                       " bytes failed: " + cudaGetErrorString(e));
+    }
+    n = c;
+    return REMAT_OK;
+  }
+};
+
+struct Events {
+  cudaEvent_t e[8] = {};
+  int create();
+  void destroy();
+};
+
+}  // namespace remat
+
+struct remat_graph_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n = 0, W = 0, Wp = 0;
+  long long TV = 0, MV = 0, maxM = 0;
+  remat::DevBuf<u64> preds, succs;
+  remat::DevBuf<long long> T, M;
+  // weight classes for the popcount form of T(X) / M(X)
+  int cls_enabled = 0, KT = 0, KM = 0;
+  remat::DevBuf<u64> clsT, clsM;
+  remat::DevBuf<long long> coefT, coefM;
+  std::vector<long long> hT, hM;
+  // evaluate / simulate scratch
+  remat::DevBuf<u64> chain_buf, bound_buf, cached_buf;
+  remat::DevBuf<long long> terms_buf, eval_out, stage_buf;
+  remat::DevBuf<int> int_buf;
+  remat::DevBuf<long long> ll_buf;
+  remat::DevBuf<int> ops_buf;
+  remat::DevBuf<long long> off_buf, trace_buf;
+  remat::DevBuf<unsigned char> runs_buf;
+  remat::Events ev;
+
+  remat::GraphView view() const {
+    return remat::GraphView{n, Wp, preds.p, succs.p, T.p, M.p};
+  }
+  remat::ClassView classes() const {
+    return remat::ClassView{cls_enabled, KT, KM, clsT.p, clsM.p, coefT.p, coefM.p};
+  }
+};
+
+struct remat_family_s {
+  remat_graph_s* g = nullptr;
+  int kind = 0;
+  long long F = 0;
+  int IB = 1;
+  remat::DevBuf<u64> masks, bound;              // SoA [Wp][F]
+  remat::DevBuf<long long> ML, TL, Mb, TLnb, base, foff;
+  long long slots = 0;
+  std::vector<long long> level_start;           // [n+2]
+  std::vector<long long> level_maxR;            // [n+1]
+  // DP state for up to nb_cap budgets
+  int nb_cap = 0;
+  remat::DevBuf<remat::Frontier> frontier;
+  remat::DevBuf<int> flen, ccount;
+  remat::DevBuf<long long> trans, budgets, results;
+  remat::DevBuf<u64> rowscratch, chain_out, cached_out;
+  remat::DevBuf<long long> stage_out, terms;
+  remat::DevBuf<int> chain_idx;
+  remat::DevBuf<u64> stage_bound;
+  remat_timings timings{};
+
+  remat::FamilyView view() const {
+    return remat::FamilyView{F, masks.p, bound.p, ML.p, TL.p, Mb.p, TLnb.p, base.p, foff.p};
+  }
+};
+
+namespace remat {
+
+// family.cu
+int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f);
+int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_t s,
+                   long long* total_host);
+
+// relax.cu
+int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,
+                remat_plan_info* info, u64* chain_masks, u64* cached_masks,
+                long long* stage_memory);
+
+// evaluate.cu: per-stage terms of chains already on device ([nb][n+1][Wp]);
+// results [nb][8]: status, k, overhead, peak, cached_total, stagewise, tstar, mfinal
+int evaluate_chains(remat_graph_s* g, int nb, const u64* chains, const int* klen,
+                    const long long* expect /*[nb][4] tstar,mfinal,budget,check or null*/,
+                    long long* stage_mem, u64* cached_masks, long long* results,
+                    long long* terms, u64* bounds);
+
+// simulate.cu
+int simulate_batch(remat_graph_s* g, int nsched, const long long* offsets_h,
+                   const int* ops_h, long long total, remat_sim_info* info,
+                   long long* traces_h);
+
+}  // namespace remat

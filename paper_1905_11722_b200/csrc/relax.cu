@@ -1,0 +1,498 @@
+// relax.cu — the DP relaxation as a level-synchronous pull wavefront (K4+K5),
+// reconstruction (K6) and the post-hoc search statistics.
+//
+// Replaces TransitionIndex pair constants (planner.py:117-132), _dp_run
+// (planner.py:145-177) and _reconstruct (180-189).
+//
+// Pull form: for target member j (|L_j| = s) and every
+// predecessor i (L_i ⊊ L_j, necessarily |L_i| < s, i.e. i < level_start[s]):
+//   candidate (t + dt_ij, m + dm_ij) from every non-dominated entry (t, m) of
+//   cell i with m + fixed_ij <= B.
+// opt[j][t2] = lexicographic min over (m2, i) — the reference's strict `<`
+// push in family order keeps the first (smallest) i among equal m2.  The
+// reduction is a 64-bit atomicMin on the packed key (m2 << IB) | i in a
+// shared-memory row over t2 ∈ [0, T(L_j)], so it is order-independent and
+// deterministic.
+//
+// Pair constants from per-member prefix terms:
+//   fixed_ij = 2(M(L_j) − M(L_i)) + stage_base_j
+//   dt_ij    = T(L_j \ ∂L_j) − T(L_i) + T(L_i ∩ ∂L_j)
+//   dm_ij    = M(∂L_j) − M(L_i ∩ ∂L_j)
+// where the two weighted popcounts of L_i ∩ ∂L_j are either a bit loop over
+// the (small) boundary or Σ_c coef_c · popc(L_i ∩ ∂L_j ∩ class_c) over the
+// graph's weight classes, whichever is cheaper for this target.
+//
+// Finalisation (K5) turns the row into the compact frontier (strict prefix-min
+// of m in t-ascending order, t-descending for maximize; planner.py:153-161)
+// and records |cell|, |frontier| and Σ_i|frontier_i| over comparable i —
+// exactly table_entries, states_visited and transitions (Appendix A.3).
+#include <algorithm>
+
+#include "device.cuh"
+
+namespace remat {
+
+template <int W>
+__global__ void __launch_bounds__(kRelaxThreads)
+    k_relax_level(FamilyView fv, GraphView g, ClassView cv, DpView dp, long long jbase,
+                  long long pred_end, int smem_row, u64* rowscratch, long long row_stride) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ int qi[kRelaxThreads];
+  __shared__ long long qfixed[kRelaxThreads], qdt[kRelaxThreads], qdm[kRelaxThreads];
+  __shared__ long long qfoff[kRelaxThreads];
+  __shared__ int qpre[kRelaxThreads + 1];
+  __shared__ u64 scr[33];
+  __shared__ u64 bjc[2 * kMaxClasses * W];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long F = fv.F;
+  const long long j = jbase + blockIdx.x;
+  const int b = blockIdx.y;
+  u64* row = smem_row ? reinterpret_cast<u64*>(smraw)
+                      : rowscratch + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * row_stride;
+
+  u64 Lj[W], Bj[W];
+  int bcnt = 0;
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    Lj[w] = fv.masks[(size_t)w * F + j];
+    Bj[w] = fv.bound[(size_t)w * F + j];
+    bcnt += __popcll(Bj[w]);
+  }
+  const long long R = fv.TL[j] + 1;
+  const long long MLj = fv.ML[j], basej = fv.base[j], TLnbj = fv.TLnb[j], Mbj = fv.Mb[j];
+  const long long B = dp.budgets[b];
+  const int IB = dp.IB;
+  const int KT = cv.KT, K = cv.KT + cv.KM;
+  const bool use_cls = cv.enabled && K * W < bcnt;
+  if (use_cls) {
+    for (int e = tid; e < K * W; e += kRelaxThreads) {
+      int c = e / W, w = e - c * W;
+      u64 cls = c < KT ? cv.clsT[c * W + w] : cv.clsM[(c - KT) * W + w];
+      bjc[e] = fv.bound[(size_t)w * F + j] & cls;
+    }
+  }
+  for (long long t = tid; t < R; t += kRelaxThreads) row[t] = ~0ull;
+  __syncthreads();
+
+  const int* flen_b = dp.flen + (size_t)b * F;
+  const long long fbase = (long long)b * dp.slots;
+  long long trans_acc = 0;
+
+  for (long long base0 = 0; base0 < pred_end; base0 += kRelaxThreads) {
+    const long long i = base0 + tid;
+    int fl = 0;
+    long long fixed = 0, dt = 0, dm = 0;
+    if (i < pred_end) {
+      u64 Li[W];
+      u64 acc = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        Li[w] = __ldg(fv.masks + (size_t)w * F + i);
+        acc |= Li[w] & ~Lj[w];
+      }
+      if (acc == 0) {
+        fl = flen_b[i];
+        if (fl > 0) {
+          long long ts = 0, ms = 0;
+          if (use_cls) {
+            for (int c = 0; c < K; c++) {
+              int pc = 0;
+#pragma unroll
+              for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bjc[c * W + w]);
+              if (c < KT) ts += __ldg(cv.coefT + c) * pc;
+              else ms += __ldg(cv.coefM + c - KT) * pc;
+            }
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+              u64 x = Li[w] & Bj[w];
+              while (x) {
+                int v = w * 64 + __ffsll((long long)x) - 1;
+                x &= x - 1;
+                ts += __ldg(g.T + v);
+                ms += __ldg(g.M + v);
+              }
+            }
+          }
+          fixed = 2 * (MLj - fv.ML[i]) + basej;
+          dt = TLnbj - fv.TL[i] + ts;
+          dm = Mbj - ms;
+        }
+      }
+    }
+    // queue the comparable predecessors with a non-empty frontier, in index order
+    u64 packed = fl > 0 ? ((1ull << 32) | (unsigned)fl) : 0ull;
+    u64 tot;
+    u64 ex = block_exclusive_sum<u64>(packed, scr, &tot);
+    const int qn = (int)(tot >> 32), total = (int)(tot & 0xffffffffu);
+    if (fl > 0) {
+      int q = (int)(ex >> 32);
+      qi[q] = (int)i;
+      qfixed[q] = fixed;
+      qdt[q] = dt;
+      qdm[q] = dm;
+      qfoff[q] = fbase + fv.foff[i];
+      qpre[q] = (int)(ex & 0xffffffffu);
+    }
+    if (tid == 0) qpre[qn] = total;
+    __syncthreads();
+    trans_acc += total;
+    // flattened (predecessor, frontier entry) items; each warp takes 32 at a time
+    for (int e0 = warp * 32; e0 < total; e0 += kRelaxThreads) {
+      int lo = 0, hi = qn - 1;
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (qpre[mid] <= e0) lo = mid; else hi = mid - 1;
+      }
+      // predecessor boundaries inside this 32-item window -> one bit each
+      int kb = lo + 1 + lane;
+      unsigned bl = kb <= qn ? (unsigned)qpre[kb] : 0xffffffffu;
+      unsigned d = bl - (unsigned)e0;
+      unsigned msk = __reduce_or_sync(kFull, d < 32u ? (1u << d) : 0u);
+      const int k = lo + __popc(msk & ((2u << lane) - 1u));
+      const int e = e0 + lane;
+      if (e < total) {
+        const Frontier fr = dp.frontier[qfoff[k] + (e - qpre[k])];
+        if (fr.m + qfixed[k] <= B) {
+          long long t2 = (long long)fr.t + qdt[k];
+          u64 key = ((u64)(fr.m + qdm[k]) << IB) | (u64)qi[k];
+          if (smem_row) {
+            // sm_100 has no native 64-bit shared-memory min (it lowers to a CAS
+            // loop); read first so losing candidates issue no atomic at all
+            u64 old = row[t2];
+            while (key < old) {
+              u64 prev = atomicCAS(row + t2, old, key);
+              if (prev == old) break;
+              old = prev;
+            }
+          } else {
+            atomicMin(row + t2, key);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- K5: frontier of cell j ----
+  const int per = (int)((R + kRelaxThreads - 1) / kRelaxThreads);
+  const long long s0 = (long long)tid * per, s1 = min(R, s0 + per);
+  const bool mx = dp.maximize;
+  u64 lmin = ~0ull;
+  unsigned cells = 0;
+  for (long long s = s0; s < s1; s++) {
+    u64 key = row[mx ? R - 1 - s : s];
+    if (key != ~0ull) {
+      cells++;
+      u64 m = key >> IB;
+      lmin = m < lmin ? m : lmin;
+    }
+  }
+  const u64 pm = block_exclusive_min(lmin, scr);
+  unsigned nf = 0;
+  u64 run = pm;
+  for (long long s = s0; s < s1; s++) {
+    u64 key = row[mx ? R - 1 - s : s];
+    if (key != ~0ull) {
+      u64 m = key >> IB;
+      if (m < run) {
+        nf++;
+        run = m;
+      }
+    }
+  }
+  u64 tot2;
+  u64 ex2 = block_exclusive_sum<u64>(((u64)cells << 32) | nf, scr, &tot2);
+  Frontier* out = dp.frontier + fbase + fv.foff[j];
+  unsigned pos = (unsigned)(ex2 & 0xffffffffu);
+  run = pm;
+  const u64 pmask = (1ull << IB) - 1;
+  for (long long s = s0; s < s1; s++) {
+    long long t = mx ? R - 1 - s : s;
+    u64 key = row[t];
+    if (key != ~0ull) {
+      u64 m = key >> IB;
+      if (m < run) {
+        Frontier f;
+        f.m = (long long)m;
+        f.t = (unsigned)t;
+        f.parent = (int)(key & pmask);
+        out[pos++] = f;
+        run = m;
+      }
+    }
+  }
+  if (tid == 0) {
+    dp.flen[(size_t)b * F + j] = (int)(tot2 & 0xffffffffu);
+    dp.ccount[(size_t)b * F + j] = (int)(tot2 >> 32);
+    dp.trans[(size_t)b * F + j] = trans_acc;
+  }
+}
+
+__global__ void k_dp_init(DpView dp, long long F, int nb) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  Frontier f;
+  f.m = 0;
+  f.t = 0;
+  f.parent = -1;
+  dp.frontier[(long long)b * dp.slots] = f;  // foff[0] == 0: the empty set
+  dp.flen[(size_t)b * F] = 1;
+  dp.ccount[(size_t)b * F] = 1;
+  dp.trans[(size_t)b * F] = 0;
+}
+
+// SearchStats, recomputed from the final table (Appendix A.3).
+__global__ void k_dp_stats(DpView dp, long long F, long long* __restrict__ out) {
+  __shared__ long long scr[3][32];
+  const int b = blockIdx.x;
+  long long sv = 0, te = 0, tr = 0;
+  for (long long i = threadIdx.x; i < F; i += blockDim.x) {
+    sv += dp.flen[(size_t)b * F + i];
+    te += dp.ccount[(size_t)b * F + i];
+    tr += dp.trans[(size_t)b * F + i];
+  }
+  sv = warp_sum(sv);
+  te = warp_sum(te);
+  tr = warp_sum(tr);
+  if ((threadIdx.x & 31) == 0) {
+    scr[0][threadIdx.x >> 5] = sv;
+    scr[1][threadIdx.x >> 5] = te;
+    scr[2][threadIdx.x >> 5] = tr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); k++) {
+      sv += scr[0][k];
+      te += scr[1][k];
+      tr += scr[2][k];
+    }
+    out[b * 4 + 0] = sv;        // states_visited
+    out[b * 4 + 1] = te;        // table_entries
+    out[b * 4 + 2] = tr;        // transitions
+    out[b * 4 + 3] = te - sv;   // dominated_skipped
+  }
+}
+
+// K6: parent walk from (V, t*) back to ∅ (planner.py:180-189), one warp per
+// budget.  Each step recomputes dt(parent, j) to recover the parent's t and
+// finds that entry in the parent's frontier with a warp-wide ballot.
+// expect[b] = {t*, m_final, budget, 1}; klen[b] = k (0 when infeasible,
+// -1 on an inconsistent table).
+template <int W>
+__global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
+                              int* __restrict__ path, u64* __restrict__ chain_out,
+                              int* __restrict__ klen, long long* __restrict__ expect) {
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const long long F = fv.F;
+  const long long fbase = (long long)b * dp.slots;
+  int* pth = path + (size_t)b * (n + 2);
+  long long j = F - 1;
+  if (dp.flen[(size_t)b * F + j] == 0) {
+    if (lane == 0) klen[b] = 0;
+    return;
+  }
+  Frontier cur = dp.frontier[fbase + fv.foff[j]];
+  if (lane == 0) {
+    expect[b * 4 + 0] = cur.t;
+    expect[b * 4 + 1] = cur.m;
+    expect[b * 4 + 2] = dp.budgets[b];
+    expect[b * 4 + 3] = 1;
+  }
+  int len = 0;
+  bool bad = false;
+  while (true) {
+    if (lane == 0) pth[len] = (int)j;
+    len++;
+    if (j == 0) break;
+    if (len > n + 1 || cur.parent < 0) {
+      bad = true;
+      break;
+    }
+    const long long par = cur.parent;
+    long long ts = 0;
+    if (lane < W)
+      ts = word_weight(fv.masks[(size_t)lane * F + par] & fv.bound[(size_t)lane * F + j], lane,
+                       g.T);
+    ts = warp_sum(ts);
+    const long long dt = fv.TLnb[j] - fv.TL[par] + ts;
+    const long long tp = (long long)cur.t - dt;
+    const int nfp = dp.flen[(size_t)b * F + par];
+    const long long pb = fbase + fv.foff[par];
+    bool found = false;
+    for (int s0 = 0; s0 < nfp && !found; s0 += 32) {
+      int s = s0 + lane;
+      bool hit = s < nfp && (long long)dp.frontier[pb + s].t == tp;
+      unsigned bal = __ballot_sync(kFull, hit);
+      if (bal) {
+        cur = dp.frontier[pb + s0 + __ffs(bal) - 1];
+        found = true;
+      }
+    }
+    if (!found) {
+      bad = true;
+      break;
+    }
+    j = par;
+  }
+  __syncwarp();
+  if (bad) {
+    if (lane == 0) klen[b] = -1;
+    return;
+  }
+  const int k = len - 1;
+  for (int s = 0; s < k; s++) {
+    int idx = pth[len - 2 - s];
+    if (lane < W)
+      chain_out[((size_t)b * (n + 1) + s) * W + lane] = fv.masks[(size_t)lane * F + idx];
+  }
+  if (lane == 0) klen[b] = k;
+}
+
+// ---------------------------------------------------------------------------
+// host driver
+// ---------------------------------------------------------------------------
+
+static constexpr int kSmemLimit = 200 * 1024;  // dynamic row bytes per CTA
+
+template <int W>
+static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int objective,
+                   remat_plan_info* info, u64* chain_masks, u64* cached_masks,
+                   long long* stage_memory) {
+  remat_graph_s* g = f->g;
+  cudaStream_t s = g->stream;
+  const int nb = (int)budgets.size();
+  const int n = g->n;
+  const long long F = f->F;
+  int rc;
+  if ((rc = f->frontier.ensure((size_t)nb * f->slots)) < 0 ||
+      (rc = f->flen.ensure((size_t)nb * F)) < 0 || (rc = f->ccount.ensure((size_t)nb * F)) < 0 ||
+      (rc = f->trans.ensure((size_t)nb * F)) < 0 || (rc = f->budgets.ensure(nb)) < 0 ||
+      (rc = f->results.ensure((size_t)nb * 20)) < 0 ||
+      (rc = f->chain_out.ensure((size_t)nb * (n + 1) * W)) < 0 ||
+      (rc = f->cached_out.ensure((size_t)nb * (n + 1) * W)) < 0 ||
+      (rc = f->stage_out.ensure((size_t)nb * (n + 1))) < 0 ||
+      (rc = f->chain_idx.ensure((size_t)nb * (n + 2) + nb)) < 0 ||
+      (rc = f->terms.ensure((size_t)nb * (n + 1) * 4)) < 0 ||
+      (rc = f->stage_bound.ensure((size_t)nb * (n + 1) * W)) < 0)
+    return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    RM_CUDA(cudaFuncSetAttribute(k_relax_level<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemLimit));
+    attr_set = true;
+  }
+  DpView dp{f->slots, f->frontier.p, f->flen.p,  f->ccount.p,
+            f->trans.p, f->budgets.p, f->IB, objective == REMAT_MAXIMIZE};
+  FamilyView fv = f->view();
+  GraphView gv = g->view();
+  ClassView cv = g->classes();
+  Events& ev = g->ev;
+  const long long launches0 = remat_kernel_launch_count();
+  RM_CUDA(cudaMemcpyAsync(f->budgets.p, budgets.data(), sizeof(long long) * nb,
+                          cudaMemcpyHostToDevice, s));
+  RM_CUDA(cudaEventRecord(ev.e[3], s));
+  k_dp_init<<<(nb + 127) / 128, 128, 0, s>>>(dp, F, nb);
+  RM_LAUNCHED();
+  long long relax_launches = 0;
+  for (int lvl = 1; lvl <= n; lvl++) {
+    const long long j0 = f->level_start[lvl], width = f->level_start[lvl + 1] - j0;
+    if (width == 0) continue;
+    const long long R = f->level_maxR[lvl];
+    const bool in_smem = R * 8 <= kSmemLimit;
+    u64* scratch = nullptr;
+    if (!in_smem) {
+      if ((rc = f->rowscratch.ensure((size_t)width * nb * R)) < 0) return rc;
+      scratch = f->rowscratch.p;
+    }
+    k_relax_level<W><<<dim3((unsigned)width, (unsigned)nb), kRelaxThreads,
+                       in_smem ? (size_t)R * 8 : 0, s>>>(fv, gv, cv, dp, j0, j0, in_smem ? 1 : 0,
+                                                         scratch, R);
+    RM_LAUNCHED();
+    relax_launches++;
+  }
+  RM_CUDA(cudaEventRecord(ev.e[4], s));
+  long long* expect = f->results.p;           // [nb][4]
+  long long* stats = f->results.p + nb * 4;   // [nb][4]
+  long long* evres = f->results.p + nb * 8;   // [nb][8]
+  int* klen = f->chain_idx.p + (size_t)nb * (n + 2);
+  k_reconstruct<W><<<nb, 32, 0, s>>>(fv, gv, dp, n, f->chain_idx.p, f->chain_out.p, klen, expect);
+  RM_LAUNCHED();
+  if ((rc = evaluate_chains(g, nb, f->chain_out.p, klen, expect, f->stage_out.p,
+                            f->cached_out.p, evres, f->terms.p, f->stage_bound.p)) < 0)
+    return rc;
+  k_dp_stats<<<nb, 1024, 0, s>>>(dp, F, stats);
+  RM_LAUNCHED();
+  RM_CUDA(cudaEventRecord(ev.e[5], s));
+  std::vector<long long> hres((size_t)nb * 16);
+  RM_CUDA(cudaMemcpyAsync(hres.data(), f->results.p, sizeof(long long) * nb * 16,
+                          cudaMemcpyDeviceToHost, s));
+  std::vector<u64> hchain, hcached;
+  std::vector<long long> hstage;
+  if (chain_masks) hchain.resize((size_t)nb * (n + 1) * W);
+  if (cached_masks) hcached.resize((size_t)nb * (n + 1) * W);
+  if (stage_memory) hstage.resize((size_t)nb * (n + 1));
+  if (chain_masks)
+    RM_CUDA(cudaMemcpyAsync(hchain.data(), f->chain_out.p, hchain.size() * 8,
+                            cudaMemcpyDeviceToHost, s));
+  if (cached_masks)
+    RM_CUDA(cudaMemcpyAsync(hcached.data(), f->cached_out.p, hcached.size() * 8,
+                            cudaMemcpyDeviceToHost, s));
+  if (stage_memory)
+    RM_CUDA(cudaMemcpyAsync(hstage.data(), f->stage_out.p, hstage.size() * 8,
+                            cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaEventRecord(ev.e[6], s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  float relax_ms = 0, finish_ms = 0, total_ms = 0;
+  cudaEventElapsedTime(&relax_ms, ev.e[3], ev.e[4]);
+  cudaEventElapsedTime(&finish_ms, ev.e[4], ev.e[5]);
+  cudaEventElapsedTime(&total_ms, ev.e[3], ev.e[6]);
+  f->timings.relax_ms = relax_ms;
+  f->timings.finish_ms = finish_ms;
+  f->timings.total_ms = total_ms;
+  f->timings.relax_launches = relax_launches;
+  f->timings.kernel_launches = remat_kernel_launch_count() - launches0;
+
+  const int Wu = g->W;
+  for (int b = 0; b < nb; b++) {
+    remat_plan_info& o = info[b];
+    const long long* st = hres.data() + nb * 4 + b * 4;
+    const long long* er = hres.data() + nb * 8 + b * 8;
+    o.stats.states_visited = st[0];
+    o.stats.table_entries = st[1];
+    o.stats.transitions = st[2];
+    o.stats.dominated_skipped = st[3];
+    o.k = (int)er[1];
+    o.status = (int)er[0];
+    o.objective_value = er[2];
+    o.overhead = er[2];
+    o.peak_memory = er[3];
+    o.cached_total = er[4];
+    const size_t rows = (size_t)(n + 1);
+    if (o.status == REMAT_OK) {
+      for (int q = 0; q < o.k; q++)
+        for (int w = 0; w < Wu; w++) {
+          size_t src = ((size_t)b * rows + q) * W + w, dst = ((size_t)b * rows + q) * Wu + w;
+          if (chain_masks) chain_masks[dst] = hchain[src];
+          if (cached_masks) cached_masks[dst] = hcached[src];
+        }
+      if (stage_memory)
+        for (int q = 0; q < o.k; q++) stage_memory[b * rows + q] = hstage[b * rows + q];
+    }
+  }
+  return REMAT_OK;
+}
+
+int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,
+                remat_plan_info* info, u64* chain_masks, u64* cached_masks,
+                long long* stage_memory) {
+  int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
+  dispatch_words(f->g->Wp, [&](auto wc) {
+    constexpr int W = decltype(wc)::value;
+    rc = solve_w<W>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
+  });
+  return rc;
+}
+
+}  // namespace remat
