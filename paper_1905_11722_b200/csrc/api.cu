@@ -16,6 +16,18 @@
 namespace remat {
 
 static thread_local std::string g_last_error;
+thread_local cudaStream_t tls_stream = nullptr;
+
+void prepare_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[device] = true;
+}
 static std::atomic<long long> g_launches{0};
 
 void set_error(int code, const std::string& msg) {
@@ -97,8 +109,10 @@ static int upload(DevBuf<long long>& d, const std::vector<long long>& h, cudaStr
   return REMAT_OK;
 }
 
-static int set_device(int dev) {
+static int set_device(int dev, cudaStream_t s = nullptr) {
   RM_CUDA(cudaSetDevice(dev));
+  prepare_pool(dev);
+  tls_stream = s;
   return REMAT_OK;
 }
 
@@ -167,6 +181,7 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
   };
   if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(fail(REMAT_ERR_CUDA, "cudaStreamCreate failed"));
+  tls_stream = g->stream;
   if ((rc = g->ev.create()) < 0) return cleanup(rc);
   std::vector<u64> hp((size_t)n * Wp, 0), hs((size_t)n * Wp, 0);
   for (int v = 0; v < n; v++)
@@ -196,12 +211,15 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
 
 int remat_graph_free(remat_graph_t g) {
   if (!g) return REMAT_OK;
-  cudaSetDevice(g->device);
-  cudaStreamSynchronize(g->stream);
+  set_device(g->device, g->stream);
   g->ev.destroy();
   cudaStream_t s = g->stream;
   delete g;
-  if (s) cudaStreamDestroy(s);
+  if (s) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+  tls_stream = nullptr;
   return REMAT_OK;
 }
 
@@ -217,7 +235,7 @@ int remat_family_create(remat_graph_t g, int32_t kind, int64_t cap, remat_family
   if (kind == REMAT_FAMILY_FULL && cap < (int64_t)g->n + 1)
     return fail(REMAT_ERR_VALUE, "cap must be at least n+1 = " + std::to_string(g->n + 1) +
                                      ", got " + std::to_string(cap));
-  int rc = set_device(g->device);
+  int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
   auto* f = new remat_family_s();
   const long long launches0 = remat_kernel_launch_count();
@@ -241,7 +259,7 @@ int remat_family_masks(remat_family_t f, int64_t start, int64_t count, uint64_t*
   if (start < 0 || count < 0 || start + count > f->F)
     return fail(REMAT_ERR_VALUE, "family index range out of bounds");
   remat_graph_s* g = f->g;
-  int rc = set_device(g->device);
+  int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
   const int W = g->W;
   std::vector<u64> tmp((size_t)count);
@@ -257,8 +275,7 @@ int remat_family_masks(remat_family_t f, int64_t start, int64_t count, uint64_t*
 
 int remat_family_free(remat_family_t f) {
   if (!f) return REMAT_OK;
-  cudaSetDevice(f->g->device);
-  cudaStreamSynchronize(f->g->stream);
+  set_device(f->g->device, f->g->stream);
   delete f;
   return REMAT_OK;
 }
@@ -275,7 +292,7 @@ int remat_solve(remat_family_t f, const int64_t* budgets, int32_t nb, int32_t ob
   if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
     return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
   remat_graph_s* g = f->g;
-  int rc = set_device(g->device);
+  int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
   std::vector<long long> bs(nb);
   for (int b = 0; b < nb; b++) {
@@ -303,7 +320,7 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
   if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
     return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
   remat_graph_s* g = f->g;
-  int rc = set_device(g->device);
+  int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
   const int K = std::max(1, std::min(probes_per_round, 64));
   const int n = g->n, W = g->W;
@@ -385,7 +402,7 @@ int remat_evaluate(remat_graph_t g, int32_t k, const uint64_t* chain, int64_t* o
                    uint64_t* cached_masks) {
   const int n = g->n, W = g->W, Wp = g->Wp;
   if (k < 1 || k > n) return fail(REMAT_ERR_VALUE, "chain length must be in [1, n]");
-  int rc = set_device(g->device);
+  int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
   const size_t rows = (size_t)(n + 1);
   std::vector<u64> hc(rows * Wp, 0);
@@ -424,7 +441,7 @@ int remat_evaluate(remat_graph_t g, int32_t k, const uint64_t* chain, int64_t* o
 int remat_simulate(remat_graph_t g, int32_t nsched, const int64_t* offsets, const int32_t* ops,
                    remat_sim_info* info, int64_t* traces) {
   if (nsched < 1) return fail(REMAT_ERR_VALUE, "need at least one schedule");
-  int rc = set_device(g->device);
+  int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
   long long total = offsets[nsched] - offsets[0];
   if (offsets[0] != 0 || total < 0) return fail(REMAT_ERR_VALUE, "bad schedule offsets");

@@ -455,14 +455,11 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
     if (F + next > Fcap) {
       long long nc = Fcap;
       while (nc < F + next) nc *= 2;
-      u64* p = nullptr;
-      cudaError_t e = cudaMalloc(&p, sizeof(u64) * W * nc);
-      if (e != cudaSuccess) return fail(REMAT_ERR_NOMEM, "family buffer allocation failed");
-      RM_CUDA(cudaMemcpyAsync(p, fam.p, sizeof(u64) * W * F, cudaMemcpyDeviceToDevice, s));
-      RM_CUDA(cudaStreamSynchronize(s));
-      cudaFree(fam.p);
-      fam.p = p;
-      fam.n = (size_t)nc * W;
+      DevBuf<u64> grown;
+      if ((rc = grown.ensure((size_t)nc * W)) < 0) return rc;
+      RM_CUDA(cudaMemcpyAsync(grown.p, fam.p, sizeof(u64) * W * F, cudaMemcpyDeviceToDevice, s));
+      std::swap(grown.p, fam.p);
+      std::swap(grown.n, fam.n);
       Fcap = nc;
     }
     level_start.push_back(F);

@@ -121,6 +121,7 @@ struct DpView {
   int* flen;                 // [nb][F]
   int* ccount;               // [nb][F]
   long long* trans;          // [nb][F]
+  int* npairs;               // [nb][F] comparable predecessors per target (P)
   const long long* budgets;  // [nb] (clamped to 2*M(V))
   int IB;                    // parent-index bits in packed row keys
   int maximize;
@@ -130,13 +131,19 @@ struct DpView {
 // host handles
 // ---------------------------------------------------------------------------
 
+// Stream the current API call works on; DevBuf allocations are stream-ordered
+// (cudaMallocAsync from the device's default pool, whose release threshold is
+// raised once per device so freed blocks are reused instead of returned).
+extern thread_local cudaStream_t tls_stream;
+void prepare_pool(int device);
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, tls_stream);
     p = nullptr;
     n = 0;
   }
@@ -144,9 +151,10 @@ struct DevBuf {
     if (count <= n && p) return REMAT_OK;
     release();
     size_t c = count ? count : 1;
-    cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), tls_stream);
     if (e != cudaSuccess) {
       p = nullptr;
+      cudaGetLastError();
       return fail(REMAT_ERR_NOMEM, "device allocation of " + std::to_string(c * sizeof(T)) +
                                        " bytes failed: " + cudaGetErrorString(e));
     }
@@ -206,8 +214,8 @@ struct remat_family_s {
   // DP state for up to nb_cap budgets
   int nb_cap = 0;
   remat::DevBuf<remat::Frontier> frontier;
-  remat::DevBuf<int> flen, ccount;
-  remat::DevBuf<long long> trans, budgets, results;
+  remat::DevBuf<int> flen, ccount, npairs;
+  remat::DevBuf<long long> trans, budgets, results, partials;
   remat::DevBuf<u64> rowscratch, chain_out, cached_out;
   remat::DevBuf<long long> stage_out, terms;
   remat::DevBuf<int> chain_idx;

@@ -32,24 +32,116 @@
 
 namespace remat {
 
+// One queued predecessor of the current chunk (32 B -> two LDS.128).
+struct __align__(16) QEntry {
+  long long foff;  // first frontier entry of the predecessor (budget-offset)
+  long long cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
+  long long dm;    // dm_ij
+  int dt;          // dt_ij (<= T(V) < 2^24)
+  int i;           // predecessor family index
+};
+
+// opt[t2] = min(opt[t2], key).  sm_100 has no native 64-bit shared-memory
+// min (it lowers to a CAS loop), so read first: a losing candidate issues no
+// atomic at all.  Global rows use the native ATOM.MIN.64.
+__device__ __forceinline__ void row_min(u64* row, long long t2, u64 key, bool smem) {
+  if (smem) {
+    u64 old = row[t2];
+    while (key < old) {
+      u64 prev = atomicCAS(row + t2, old, key);
+      if (prev == old) break;
+      old = prev;
+    }
+  } else {
+    atomicMin(row + t2, key);
+  }
+}
+
+// K5 on a finished row: |cell|, the strict prefix-min frontier in t order
+// (ascending for minimize, descending for maximize; planner.py:153-161),
+// compacted into the member's frontier slot with its back-pointers.
+__device__ void finalize_row(const u64* row, long long R, const DpView& dp, const FamilyView& fv,
+                             long long j, int b, long long trans_acc, long long pairs_acc,
+                             u64* scr) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const long long F = fv.F;
+  const int IB = dp.IB;
+  const int per = (int)((R + nt - 1) / nt);
+  const long long s0 = (long long)tid * per, s1 = min(R, s0 + per);
+  const bool mx = dp.maximize;
+  u64 lmin = ~0ull;
+  unsigned cells = 0;
+  for (long long s = s0; s < s1; s++) {
+    u64 key = row[mx ? R - 1 - s : s];
+    if (key != ~0ull) {
+      cells++;
+      u64 m = key >> IB;
+      lmin = m < lmin ? m : lmin;
+    }
+  }
+  const u64 pm = block_exclusive_min(lmin, scr);
+  unsigned nf = 0;
+  u64 run = pm;
+  for (long long s = s0; s < s1; s++) {
+    u64 key = row[mx ? R - 1 - s : s];
+    if (key != ~0ull) {
+      u64 m = key >> IB;
+      if (m < run) {
+        nf++;
+        run = m;
+      }
+    }
+  }
+  u64 tot2;
+  u64 ex2 = block_exclusive_sum<u64>(((u64)cells << 32) | nf, scr, &tot2);
+  Frontier* out = dp.frontier + (long long)b * dp.slots + fv.foff[j];
+  unsigned pos = (unsigned)(ex2 & 0xffffffffu);
+  run = pm;
+  const u64 pmask = (1ull << IB) - 1;
+  for (long long s = s0; s < s1; s++) {
+    long long t = mx ? R - 1 - s : s;
+    u64 key = row[t];
+    if (key != ~0ull) {
+      u64 m = key >> IB;
+      if (m < run) {
+        Frontier f;
+        f.m = (long long)m;
+        f.t = (unsigned)t;
+        f.parent = (int)(key & pmask);
+        out[pos++] = f;
+        run = m;
+      }
+    }
+  }
+  if (tid == 0) {
+    dp.flen[(size_t)b * F + j] = (int)(tot2 & 0xffffffffu);
+    dp.ccount[(size_t)b * F + j] = (int)(tot2 >> 32);
+    dp.trans[(size_t)b * F + j] = trans_acc;
+    dp.npairs[(size_t)b * F + j] = (int)pairs_acc;
+  }
+}
+
+// K4 (+K5 when unsplit).  Grid: (width·splits, nb); CTA (target tj, slice)
+// scans predecessor chunks [slice·nch/splits, (slice+1)·nch/splits).
 template <int W>
 __global__ void __launch_bounds__(kRelaxThreads)
     k_relax_level(FamilyView fv, GraphView g, ClassView cv, DpView dp, long long jbase,
-                  long long pred_end, int smem_row, u64* rowscratch, long long row_stride) {
+                  long long pred_end, int splits, int smem_row, u64* grow, long long grow_stride,
+                  long long* part) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ int qi[kRelaxThreads];
-  __shared__ long long qfixed[kRelaxThreads], qdt[kRelaxThreads], qdm[kRelaxThreads];
-  __shared__ long long qfoff[kRelaxThreads];
+  __shared__ QEntry q[kRelaxThreads];
   __shared__ int qpre[kRelaxThreads + 1];
   __shared__ u64 scr[33];
   __shared__ u64 bjc[2 * kMaxClasses * W];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long F = fv.F;
-  const long long j = jbase + blockIdx.x;
+  const int width = gridDim.x / splits;
+  const int tj = blockIdx.x / splits, slice = blockIdx.x - tj * splits;
+  const long long j = jbase + tj;
   const int b = blockIdx.y;
-  u64* row = smem_row ? reinterpret_cast<u64*>(smraw)
-                      : rowscratch + ((long long)blockIdx.y * gridDim.x + blockIdx.x) * row_stride;
+  u64* grow_j = grow ? grow + ((long long)b * width + tj) * grow_stride : nullptr;
+  u64* row = smem_row ? reinterpret_cast<u64*>(smraw) : grow_j;
 
   u64 Lj[W], Bj[W];
   int bcnt = 0;
@@ -72,16 +164,20 @@ __global__ void __launch_bounds__(kRelaxThreads)
       bjc[e] = fv.bound[(size_t)w * F + j] & cls;
     }
   }
-  for (long long t = tid; t < R; t += kRelaxThreads) row[t] = ~0ull;
+  if (smem_row)
+    for (long long t = tid; t < R; t += kRelaxThreads) row[t] = ~0ull;
   __syncthreads();
 
   const int* flen_b = dp.flen + (size_t)b * F;
   const long long fbase = (long long)b * dp.slots;
-  long long trans_acc = 0;
+  long long trans_acc = 0, pairs_acc = 0;
+  const long long nch = (pred_end + kRelaxThreads - 1) / kRelaxThreads;
+  const long long c0 = slice * nch / splits, c1 = (slice + 1) * nch / splits;
 
-  for (long long base0 = 0; base0 < pred_end; base0 += kRelaxThreads) {
-    const long long i = base0 + tid;
+  for (long long ch = c0; ch < c1; ch++) {
+    const long long i = ch * kRelaxThreads + tid;
     int fl = 0;
+    bool comparable = false;
     long long fixed = 0, dt = 0, dm = 0;
     if (i < pred_end) {
       u64 Li[W];
@@ -91,7 +187,8 @@ __global__ void __launch_bounds__(kRelaxThreads)
         Li[w] = __ldg(fv.masks + (size_t)w * F + i);
         acc |= Li[w] & ~Lj[w];
       }
-      if (acc == 0) {
+      comparable = acc == 0;
+      if (comparable) {
         fl = flen_b[i];
         if (fl > 0) {
           long long ts = 0, ms = 0;
@@ -127,107 +224,86 @@ __global__ void __launch_bounds__(kRelaxThreads)
     u64 ex = block_exclusive_sum<u64>(packed, scr, &tot);
     const int qn = (int)(tot >> 32), total = (int)(tot & 0xffffffffu);
     if (fl > 0) {
-      int q = (int)(ex >> 32);
-      qi[q] = (int)i;
-      qfixed[q] = fixed;
-      qdt[q] = dt;
-      qdm[q] = dm;
-      qfoff[q] = fbase + fv.foff[i];
-      qpre[q] = (int)(ex & 0xffffffffu);
+      int qp = (int)(ex >> 32);
+      QEntry e;
+      e.foff = fbase + fv.foff[i];
+      e.cap = B - fixed;
+      e.dm = dm;
+      e.dt = (int)dt;
+      e.i = (int)i;
+      q[qp] = e;
+      qpre[qp] = (int)(ex & 0xffffffffu);
     }
     if (tid == 0) qpre[qn] = total;
-    __syncthreads();
+    pairs_acc += __syncthreads_count(comparable);
     trans_acc += total;
-    // flattened (predecessor, frontier entry) items; each warp takes 32 at a time
-    for (int e0 = warp * 32; e0 < total; e0 += kRelaxThreads) {
+    // Flattened (predecessor, frontier entry) items.  Warp w takes the
+    // contiguous range [w·per, (w+1)·per); one binary search finds its first
+    // predecessor, then each 32-item window maps lanes to predecessors with
+    // one ballot over the window's predecessor boundaries.
+    const int per = ((total + kRelaxWarps - 1) / kRelaxWarps + 31) & ~31;
+    const int eb = warp * per, ee = min(total, eb + per);
+    if (eb < ee) {
       int lo = 0, hi = qn - 1;
       while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
-        if (qpre[mid] <= e0) lo = mid; else hi = mid - 1;
+        if (qpre[mid] <= eb) lo = mid; else hi = mid - 1;
       }
-      // predecessor boundaries inside this 32-item window -> one bit each
-      int kb = lo + 1 + lane;
-      unsigned bl = kb <= qn ? (unsigned)qpre[kb] : 0xffffffffu;
-      unsigned d = bl - (unsigned)e0;
-      unsigned msk = __reduce_or_sync(kFull, d < 32u ? (1u << d) : 0u);
-      const int k = lo + __popc(msk & ((2u << lane) - 1u));
-      const int e = e0 + lane;
-      if (e < total) {
-        const Frontier fr = dp.frontier[qfoff[k] + (e - qpre[k])];
-        if (fr.m + qfixed[k] <= B) {
-          long long t2 = (long long)fr.t + qdt[k];
-          u64 key = ((u64)(fr.m + qdm[k]) << IB) | (u64)qi[k];
-          if (smem_row) {
-            // sm_100 has no native 64-bit shared-memory min (it lowers to a CAS
-            // loop); read first so losing candidates issue no atomic at all
-            u64 old = row[t2];
-            while (key < old) {
-              u64 prev = atomicCAS(row + t2, old, key);
-              if (prev == old) break;
-              old = prev;
-            }
-          } else {
-            atomicMin(row + t2, key);
+      int k0 = lo;
+      for (int e0 = eb; e0 < ee; e0 += 32) {
+        int kb = k0 + 1 + lane;
+        unsigned bl = kb <= qn ? (unsigned)qpre[kb] : 0xffffffffu;
+        unsigned d = bl - (unsigned)e0;
+        unsigned msk = __reduce_or_sync(kFull, d < 32u ? (1u << d) : 0u);
+        const int k = k0 + __popc(msk & ((2u << lane) - 1u));
+        const int e = e0 + lane;
+        if (e < ee) {
+          const QEntry qe = q[k];
+          const Frontier fr = dp.frontier[qe.foff + (e - qpre[k])];
+          if (fr.m <= qe.cap) {
+            u64 key = ((u64)(fr.m + qe.dm) << IB) | (u64)qe.i;
+            row_min(row, (long long)fr.t + qe.dt, key, smem_row);
           }
         }
+        k0 += __popc(msk);
+        if (k0 < qn && qpre[k0 + 1] <= e0 + 32) k0++;
       }
     }
     __syncthreads();
   }
 
-  // ---- K5: frontier of cell j ----
-  const int per = (int)((R + kRelaxThreads - 1) / kRelaxThreads);
-  const long long s0 = (long long)tid * per, s1 = min(R, s0 + per);
-  const bool mx = dp.maximize;
-  u64 lmin = ~0ull;
-  unsigned cells = 0;
-  for (long long s = s0; s < s1; s++) {
-    u64 key = row[mx ? R - 1 - s : s];
-    if (key != ~0ull) {
-      cells++;
-      u64 m = key >> IB;
-      lmin = m < lmin ? m : lmin;
-    }
+  if (splits == 1 && smem_row) {
+    finalize_row(row, R, dp, fv, j, b, trans_acc, pairs_acc, scr);
+    return;
   }
-  const u64 pm = block_exclusive_min(lmin, scr);
-  unsigned nf = 0;
-  u64 run = pm;
-  for (long long s = s0; s < s1; s++) {
-    u64 key = row[mx ? R - 1 - s : s];
-    if (key != ~0ull) {
-      u64 m = key >> IB;
-      if (m < run) {
-        nf++;
-        run = m;
-      }
+  if (smem_row)  // fold this slice's row into the target's global row
+    for (long long t = tid; t < R; t += kRelaxThreads) {
+      u64 key = row[t];
+      if (key != ~0ull) atomicMin(grow_j + t, key);
     }
-  }
-  u64 tot2;
-  u64 ex2 = block_exclusive_sum<u64>(((u64)cells << 32) | nf, scr, &tot2);
-  Frontier* out = dp.frontier + fbase + fv.foff[j];
-  unsigned pos = (unsigned)(ex2 & 0xffffffffu);
-  run = pm;
-  const u64 pmask = (1ull << IB) - 1;
-  for (long long s = s0; s < s1; s++) {
-    long long t = mx ? R - 1 - s : s;
-    u64 key = row[t];
-    if (key != ~0ull) {
-      u64 m = key >> IB;
-      if (m < run) {
-        Frontier f;
-        f.m = (long long)m;
-        f.t = (unsigned)t;
-        f.parent = (int)(key & pmask);
-        out[pos++] = f;
-        run = m;
-      }
-    }
-  }
   if (tid == 0) {
-    dp.flen[(size_t)b * F + j] = (int)(tot2 & 0xffffffffu);
-    dp.ccount[(size_t)b * F + j] = (int)(tot2 >> 32);
-    dp.trans[(size_t)b * F + j] = trans_acc;
+    long long* pp = part + (((long long)b * width + tj) * splits + slice) * 2;
+    pp[0] = trans_acc;
+    pp[1] = pairs_acc;
   }
+}
+
+// K5 for split / global-row levels: one CTA per (target, budget).
+__global__ void __launch_bounds__(kRelaxThreads)
+    k_finalize_level(FamilyView fv, DpView dp, long long jbase, int width, int splits,
+                     const u64* __restrict__ grow, long long grow_stride,
+                     const long long* __restrict__ part) {
+  __shared__ u64 scr[33];
+  const int tj = blockIdx.x, b = blockIdx.y;
+  const long long j = jbase + tj;
+  long long tr = 0, pr = 0;
+  const long long* pp = part + ((long long)b * width + tj) * splits * 2;
+  for (int s = 0; s < splits; s++) {
+    tr += pp[2 * s];
+    pr += pp[2 * s + 1];
+  }
+  finalize_row(grow + ((long long)b * width + tj) * grow_stride, fv.TL[j] + 1, dp, fv, j, b, tr,
+               pr, scr);
 }
 
 __global__ void k_dp_init(DpView dp, long long F, int nb) {
@@ -241,25 +317,29 @@ __global__ void k_dp_init(DpView dp, long long F, int nb) {
   dp.flen[(size_t)b * F] = 1;
   dp.ccount[(size_t)b * F] = 1;
   dp.trans[(size_t)b * F] = 0;
+  dp.npairs[(size_t)b * F] = 0;
 }
 
 // SearchStats, recomputed from the final table (Appendix A.3).
 __global__ void k_dp_stats(DpView dp, long long F, long long* __restrict__ out) {
-  __shared__ long long scr[3][32];
+  __shared__ long long scr[4][32];
   const int b = blockIdx.x;
-  long long sv = 0, te = 0, tr = 0;
+  long long sv = 0, te = 0, tr = 0, np = 0;
   for (long long i = threadIdx.x; i < F; i += blockDim.x) {
     sv += dp.flen[(size_t)b * F + i];
     te += dp.ccount[(size_t)b * F + i];
     tr += dp.trans[(size_t)b * F + i];
+    np += dp.npairs[(size_t)b * F + i];
   }
   sv = warp_sum(sv);
   te = warp_sum(te);
   tr = warp_sum(tr);
+  np = warp_sum(np);
   if ((threadIdx.x & 31) == 0) {
     scr[0][threadIdx.x >> 5] = sv;
     scr[1][threadIdx.x >> 5] = te;
     scr[2][threadIdx.x >> 5] = tr;
+    scr[3][threadIdx.x >> 5] = np;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -267,11 +347,13 @@ __global__ void k_dp_stats(DpView dp, long long F, long long* __restrict__ out) 
       sv += scr[0][k];
       te += scr[1][k];
       tr += scr[2][k];
+      np += scr[3][k];
     }
-    out[b * 4 + 0] = sv;        // states_visited
-    out[b * 4 + 1] = te;        // table_entries
-    out[b * 4 + 2] = tr;        // transitions
-    out[b * 4 + 3] = te - sv;   // dominated_skipped
+    out[b * 5 + 0] = sv;        // states_visited
+    out[b * 5 + 1] = te;        // table_entries
+    out[b * 5 + 2] = tr;        // transitions
+    out[b * 5 + 3] = te - sv;   // dominated_skipped
+    out[b * 5 + 4] = np;        // comparable pairs P
   }
 }
 
@@ -369,6 +451,7 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   if ((rc = f->frontier.ensure((size_t)nb * f->slots)) < 0 ||
       (rc = f->flen.ensure((size_t)nb * F)) < 0 || (rc = f->ccount.ensure((size_t)nb * F)) < 0 ||
       (rc = f->trans.ensure((size_t)nb * F)) < 0 || (rc = f->budgets.ensure(nb)) < 0 ||
+      (rc = f->npairs.ensure((size_t)nb * F)) < 0 ||
       (rc = f->results.ensure((size_t)nb * 20)) < 0 ||
       (rc = f->chain_out.ensure((size_t)nb * (n + 1) * W)) < 0 ||
       (rc = f->cached_out.ensure((size_t)nb * (n + 1) * W)) < 0 ||
@@ -383,8 +466,8 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
                                  kSmemLimit));
     attr_set = true;
   }
-  DpView dp{f->slots, f->frontier.p, f->flen.p,  f->ccount.p,
-            f->trans.p, f->budgets.p, f->IB, objective == REMAT_MAXIMIZE};
+  DpView dp{f->slots,    f->frontier.p, f->flen.p, f->ccount.p, f->trans.p,
+            f->npairs.p, f->budgets.p,  f->IB,     objective == REMAT_MAXIMIZE};
   FamilyView fv = f->view();
   GraphView gv = g->view();
   ClassView cv = g->classes();
@@ -396,26 +479,44 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   k_dp_init<<<(nb + 127) / 128, 128, 0, s>>>(dp, F, nb);
   RM_LAUNCHED();
   long long relax_launches = 0;
+  static int num_sms = 0;
+  if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  const long long target_ctas = (long long)num_sms * 4;  // resident CTAs at 256 threads
   for (int lvl = 1; lvl <= n; lvl++) {
     const long long j0 = f->level_start[lvl], width = f->level_start[lvl + 1] - j0;
     if (width == 0) continue;
     const long long R = f->level_maxR[lvl];
     const bool in_smem = R * 8 <= kSmemLimit;
-    u64* scratch = nullptr;
-    if (!in_smem) {
-      if ((rc = f->rowscratch.ensure((size_t)width * nb * R)) < 0) return rc;
-      scratch = f->rowscratch.p;
+    const long long nch = (j0 + kRelaxThreads - 1) / kRelaxThreads;
+    // split the predecessor scan across CTAs when the level alone cannot fill
+    // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
+    long long splits = (target_ctas + width * nb - 1) / (width * nb);
+    splits = std::max(1LL, std::min(splits, nch / 2));
+    u64* grow = nullptr;
+    long long* part = nullptr;
+    if (splits > 1 || !in_smem) {
+      if ((rc = f->rowscratch.ensure((size_t)width * nb * R)) < 0 ||
+          (rc = f->partials.ensure((size_t)width * nb * splits * 2)) < 0)
+        return rc;
+      grow = f->rowscratch.p;
+      part = f->partials.p;
+      RM_CUDA(cudaMemsetAsync(grow, 0xff, sizeof(u64) * width * nb * R, s));
     }
-    k_relax_level<W><<<dim3((unsigned)width, (unsigned)nb), kRelaxThreads,
-                       in_smem ? (size_t)R * 8 : 0, s>>>(fv, gv, cv, dp, j0, j0, in_smem ? 1 : 0,
-                                                         scratch, R);
+    k_relax_level<W><<<dim3((unsigned)(width * splits), (unsigned)nb), kRelaxThreads,
+                       in_smem ? (size_t)R * 8 : 0, s>>>(fv, gv, cv, dp, j0, j0, (int)splits,
+                                                         in_smem ? 1 : 0, grow, R, part);
     RM_LAUNCHED();
     relax_launches++;
+    if (grow) {
+      k_finalize_level<<<dim3((unsigned)width, (unsigned)nb), kRelaxThreads, 0, s>>>(
+          fv, dp, j0, (int)width, (int)splits, grow, R, part);
+      RM_LAUNCHED();
+    }
   }
   RM_CUDA(cudaEventRecord(ev.e[4], s));
   long long* expect = f->results.p;           // [nb][4]
-  long long* stats = f->results.p + nb * 4;   // [nb][4]
-  long long* evres = f->results.p + nb * 8;   // [nb][8]
+  long long* stats = f->results.p + nb * 4;   // [nb][5]
+  long long* evres = f->results.p + nb * 9;   // [nb][8]
   int* klen = f->chain_idx.p + (size_t)nb * (n + 2);
   k_reconstruct<W><<<nb, 32, 0, s>>>(fv, gv, dp, n, f->chain_idx.p, f->chain_out.p, klen, expect);
   RM_LAUNCHED();
@@ -425,8 +526,8 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   k_dp_stats<<<nb, 1024, 0, s>>>(dp, F, stats);
   RM_LAUNCHED();
   RM_CUDA(cudaEventRecord(ev.e[5], s));
-  std::vector<long long> hres((size_t)nb * 16);
-  RM_CUDA(cudaMemcpyAsync(hres.data(), f->results.p, sizeof(long long) * nb * 16,
+  std::vector<long long> hres((size_t)nb * 17);
+  RM_CUDA(cudaMemcpyAsync(hres.data(), f->results.p, sizeof(long long) * nb * 17,
                           cudaMemcpyDeviceToHost, s));
   std::vector<u64> hchain, hcached;
   std::vector<long long> hstage;
@@ -457,8 +558,9 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   const int Wu = g->W;
   for (int b = 0; b < nb; b++) {
     remat_plan_info& o = info[b];
-    const long long* st = hres.data() + nb * 4 + b * 4;
-    const long long* er = hres.data() + nb * 8 + b * 8;
+    const long long* st = hres.data() + nb * 4 + b * 5;
+    const long long* er = hres.data() + nb * 9 + b * 8;
+    if (b == 0) f->timings.comparable_pairs = st[4];
     o.stats.states_visited = st[0];
     o.stats.table_entries = st[1];
     o.stats.transitions = st[2];
