@@ -33,6 +33,8 @@
 namespace remat {
 
 // One queued predecessor of the current chunk (32 B -> two LDS.128).
+constexpr int kMapCap = 4096;  // items per round of the item -> predecessor map
+
 struct __align__(16) QEntry {
   long long foff;  // first frontier entry of the predecessor (budget-offset)
   long long cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
@@ -131,10 +133,11 @@ __global__ void __launch_bounds__(kRelaxThreads)
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ QEntry q[kRelaxThreads];
   __shared__ int qpre[kRelaxThreads + 1];
+  __shared__ unsigned short qmap[kMapCap];
   __shared__ u64 scr[33];
   __shared__ u64 bjc[2 * kMaxClasses * W];
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const long long F = fv.F;
   const int width = gridDim.x / splits;
   const int tj = blockIdx.x / splits, slice = blockIdx.x - tj * splits;
@@ -237,39 +240,29 @@ __global__ void __launch_bounds__(kRelaxThreads)
     if (tid == 0) qpre[qn] = total;
     pairs_acc += __syncthreads_count(comparable);
     trans_acc += total;
-    // Flattened (predecessor, frontier entry) items.  Warp w takes the
-    // contiguous range [w·per, (w+1)·per); one binary search finds its first
-    // predecessor, then each 32-item window maps lanes to predecessors with
-    // one ballot over the window's predecessor boundaries.
-    const int per = ((total + kRelaxWarps - 1) / kRelaxWarps + 31) & ~31;
-    const int eb = warp * per, ee = min(total, eb + per);
-    if (eb < ee) {
-      int lo = 0, hi = qn - 1;
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (qpre[mid] <= eb) lo = mid; else hi = mid - 1;
+    // Flattened (predecessor, frontier entry) items, in rounds of kMapCap:
+    // every queued predecessor stamps its index over its item range of an
+    // item -> predecessor map, so each item is independent (one LDS for its
+    // predecessor) and a thread keeps several frontier loads in flight.
+    for (int r0 = 0; r0 < total; r0 += kMapCap) {
+      const int r1 = min(total, r0 + kMapCap);
+      if (tid < qn) {
+        const int a = max(qpre[tid], r0), z = min(qpre[tid + 1], r1);
+        for (int e = a; e < z; e++) qmap[e - r0] = (unsigned short)tid;
       }
-      int k0 = lo;
-      for (int e0 = eb; e0 < ee; e0 += 32) {
-        int kb = k0 + 1 + lane;
-        unsigned bl = kb <= qn ? (unsigned)qpre[kb] : 0xffffffffu;
-        unsigned d = bl - (unsigned)e0;
-        unsigned msk = __reduce_or_sync(kFull, d < 32u ? (1u << d) : 0u);
-        const int k = k0 + __popc(msk & ((2u << lane) - 1u));
-        const int e = e0 + lane;
-        if (e < ee) {
-          const QEntry qe = q[k];
-          const Frontier fr = dp.frontier[qe.foff + (e - qpre[k])];
-          if (fr.m <= qe.cap) {
-            u64 key = ((u64)(fr.m + qe.dm) << IB) | (u64)qe.i;
-            row_min(row, (long long)fr.t + qe.dt, key, smem_row);
-          }
+      __syncthreads();
+#pragma unroll 4
+      for (int e = r0 + tid; e < r1; e += kRelaxThreads) {
+        const int k = qmap[e - r0];
+        const QEntry qe = q[k];
+        const Frontier fr = dp.frontier[qe.foff + (e - qpre[k])];
+        if (fr.m <= qe.cap) {
+          u64 key = ((u64)(fr.m + qe.dm) << IB) | (u64)qe.i;
+          row_min(row, (long long)fr.t + qe.dt, key, smem_row);
         }
-        k0 += __popc(msk);
-        if (k0 < qn && qpre[k0 + 1] <= e0 + 32) k0++;
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
 
   if (splits == 1 && smem_row) {
