@@ -33,7 +33,7 @@
 namespace remat {
 
 // One queued predecessor of the current chunk (32 B -> two LDS.128).
-constexpr int kMapCap = 4096;  // items per round of the item -> predecessor map
+constexpr int kWarpMap = 512;  // items per round of a warp's item -> predecessor map
 
 struct __align__(16) QEntry {
   long long foff;  // first frontier entry of the predecessor (budget-offset)
@@ -124,20 +124,26 @@ __device__ void finalize_row(const u64* row, long long R, const DpView& dp, cons
 }
 
 // K4 (+K5 when unsplit).  Grid: (width·splits, nb); CTA (target tj, slice)
-// scans predecessor chunks [slice·nch/splits, (slice+1)·nch/splits).
+// scans the predecessors [slice·P/splits, (slice+1)·P/splits) in 32-member
+// chunks.  Warps work independently (no block barrier in the main loop): a
+// warp tests 32 predecessors (lane = predecessor), queues the comparable ones
+// with a non-empty frontier in its private queue, stamps an item ->
+// predecessor map, and relaxes the flattened (predecessor, frontier entry)
+// items with its 32 lanes into the CTA's shared row.
 template <int W>
 __global__ void __launch_bounds__(kRelaxThreads)
     k_relax_level(FamilyView fv, GraphView g, ClassView cv, DpView dp, long long jbase,
                   long long pred_end, int splits, int smem_row, u64* grow, long long grow_stride,
                   long long* part) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ QEntry q[kRelaxThreads];
-  __shared__ int qpre[kRelaxThreads + 1];
-  __shared__ unsigned short qmap[kMapCap];
+  __shared__ QEntry wq[kRelaxWarps][32];
+  __shared__ int wpre[kRelaxWarps][33];
+  __shared__ unsigned short wmap[kRelaxWarps][kWarpMap];
   __shared__ u64 scr[33];
+  __shared__ long long red[2][kRelaxWarps];
   __shared__ u64 bjc[2 * kMaxClasses * W];
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long F = fv.F;
   const int width = gridDim.x / splits;
   const int tj = blockIdx.x / splits, slice = blockIdx.x - tj * splits;
@@ -174,11 +180,14 @@ __global__ void __launch_bounds__(kRelaxThreads)
   const int* flen_b = dp.flen + (size_t)b * F;
   const long long fbase = (long long)b * dp.slots;
   long long trans_acc = 0, pairs_acc = 0;
-  const long long nch = (pred_end + kRelaxThreads - 1) / kRelaxThreads;
+  const long long nch = (pred_end + 31) / 32;
   const long long c0 = slice * nch / splits, c1 = (slice + 1) * nch / splits;
+  QEntry* q = wq[warp];
+  int* qpre = wpre[warp];
+  unsigned short* qmap = wmap[warp];
 
-  for (long long ch = c0; ch < c1; ch++) {
-    const long long i = ch * kRelaxThreads + tid;
+  for (long long ch = c0 + warp; ch < c1; ch += kRelaxWarps) {
+    const long long i = ch * 32 + lane;
     int fl = 0;
     bool comparable = false;
     long long fixed = 0, dt = 0, dm = 0;
@@ -221,13 +230,15 @@ __global__ void __launch_bounds__(kRelaxThreads)
         }
       }
     }
-    // queue the comparable predecessors with a non-empty frontier, in index order
-    u64 packed = fl > 0 ? ((1ull << 32) | (unsigned)fl) : 0ull;
-    u64 tot;
-    u64 ex = block_exclusive_sum<u64>(packed, scr, &tot);
-    const int qn = (int)(tot >> 32), total = (int)(tot & 0xffffffffu);
+    const unsigned has = __ballot_sync(kFull, fl > 0);
+    pairs_acc += __popc(__ballot_sync(kFull, comparable));
+    if (!has) continue;
+    const int qn = __popc(has);
+    const int incl = warp_inclusive_sum(fl);
+    const int total = __shfl_sync(kFull, incl, 31);
+    trans_acc += total;
     if (fl > 0) {
-      int qp = (int)(ex >> 32);
+      const int qp = __popc(has & ((1u << lane) - 1));
       QEntry e;
       e.foff = fbase + fv.foff[i];
       e.cap = B - fixed;
@@ -235,24 +246,19 @@ __global__ void __launch_bounds__(kRelaxThreads)
       e.dt = (int)dt;
       e.i = (int)i;
       q[qp] = e;
-      qpre[qp] = (int)(ex & 0xffffffffu);
+      qpre[qp] = incl - fl;
     }
-    if (tid == 0) qpre[qn] = total;
-    pairs_acc += __syncthreads_count(comparable);
-    trans_acc += total;
-    // Flattened (predecessor, frontier entry) items, in rounds of kMapCap:
-    // every queued predecessor stamps its index over its item range of an
-    // item -> predecessor map, so each item is independent (one LDS for its
-    // predecessor) and a thread keeps several frontier loads in flight.
-    for (int r0 = 0; r0 < total; r0 += kMapCap) {
-      const int r1 = min(total, r0 + kMapCap);
-      if (tid < qn) {
-        const int a = max(qpre[tid], r0), z = min(qpre[tid + 1], r1);
-        for (int e = a; e < z; e++) qmap[e - r0] = (unsigned short)tid;
+    if (lane == 0) qpre[qn] = total;
+    __syncwarp();
+    for (int r0 = 0; r0 < total; r0 += kWarpMap) {
+      const int r1 = min(total, r0 + kWarpMap);
+      if (lane < qn) {
+        const int a = max(qpre[lane], r0), z = min(qpre[lane + 1], r1);
+        for (int e = a; e < z; e++) qmap[e - r0] = (unsigned short)lane;
       }
-      __syncthreads();
+      __syncwarp();
 #pragma unroll 4
-      for (int e = r0 + tid; e < r1; e += kRelaxThreads) {
+      for (int e = r0 + lane; e < r1; e += 32) {
         const int k = qmap[e - r0];
         const QEntry qe = q[k];
         const Frontier fr = dp.frontier[qe.foff + (e - qpre[k])];
@@ -261,10 +267,21 @@ __global__ void __launch_bounds__(kRelaxThreads)
           row_min(row, (long long)fr.t + qe.dt, key, smem_row);
         }
       }
-      __syncthreads();
+      __syncwarp();
     }
   }
-
+  // per-CTA totals (trans_acc is warp-uniform; pairs_acc too)
+  if (lane == 0) {
+    red[0][warp] = trans_acc;
+    red[1][warp] = pairs_acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kRelaxWarps; w++) {
+      trans_acc += red[0][w];
+      pairs_acc += red[1][w];
+    }
+  }
   if (splits == 1 && smem_row) {
     finalize_row(row, R, dp, fv, j, b, trans_acc, pairs_acc, scr);
     return;
