@@ -11,6 +11,7 @@
 // exactly once, so no hash/dedup is needed; each level is then ranked by mask
 // value, which reproduces the reference order (popcount, mask).
 #include <algorithm>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -587,6 +588,11 @@ int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
     return fail(REMAT_ERR_RANGE, "total memory cost " + std::to_string(g->MV) +
                                      " too large for packed DP keys with a family of " +
                                      std::to_string(f->F) + " members");
+  // 32-bit keys hold (m2 << IB) | i for every m2 <= M(V) strictly below the
+  // empty-slot sentinel 0xffffffff
+  f->narrow = ((unsigned long long)(g->MV + 1) << ib) < (1ull << 32);
+  if (const char* e = getenv("REMAT_FORCE_WIDE"))
+    if (e[0] == '1') f->narrow = 0;
   return REMAT_OK;
 }
 

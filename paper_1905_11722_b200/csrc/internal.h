@@ -7,9 +7,13 @@
 //            warp reading 32 consecutive members' word w is one coalesced
 //            256-byte transaction), per-member int64 scalars ML, TL, Mb, TLnb,
 //            base, frontier slot offsets foff[F+1]
-//   DP:      per budget b: Frontier entries (16 B) in slots
+//   DP:      per budget b: frontier entries in slots
 //            [b*slots + foff[j], b*slots + foff[j+1]) — capacity T(L_j)+1, the
-//            dense row length — plus flen/ccount/trans [nb][F].
+//            dense row length.  Entries are 8 B {t:u32, m:u32} when the packed
+//            row key (m << IB | i) fits 32 bits ("narrow", every named config),
+//            else 16 B {t:u32, pad, m:i64}; back-pointers live in a parallel
+//            int32 array (read only by reconstruction).  Per (budget, member):
+//            flen, ccount, mmin (smallest m = last stored entry), trans, npairs.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -30,12 +34,16 @@ constexpr int kMaxClasses = 32;      // weight classes per cost vector
 constexpr int kRelaxThreads = 256;
 constexpr int kRelaxWarps = kRelaxThreads / 32;
 
-// One non-dominated DP entry (t, m) of a member plus its back-pointer
-// (DpTable.opt / parent, reference planner.py:82-92).  16 bytes -> one LDG.128.
-struct __align__(16) Frontier {
-  long long m;     // cached memory (opt value)
-  unsigned t;      // accumulated overhead
-  int parent;      // family index of the predecessor cell (-1 for ∅)
+// One non-dominated DP entry (t, m) of a member (DpTable.opt, reference
+// planner.py:82-92); the back-pointer (DpTable.parent) is stored apart.
+struct __align__(8) EntryN {   // narrow: one LDG.64
+  unsigned t;  // accumulated overhead
+  unsigned m;  // cached memory
+};
+struct __align__(16) EntryW {  // wide: one LDG.128
+  unsigned t;
+  unsigned pad;
+  long long m;
 };
 
 // Words per set, padded to an instantiated width.
@@ -117,11 +125,13 @@ struct ClassView {
 
 struct DpView {
   long long slots;           // frontier slots per budget
-  Frontier* frontier;        // [nb][slots]
-  int* flen;                 // [nb][F]
-  int* ccount;               // [nb][F]
-  long long* trans;          // [nb][F]
-  int* npairs;               // [nb][F] comparable predecessors per target (P)
+  void* fe;                  // [nb][slots] EntryN or EntryW
+  int* parent;               // [nb][slots] family index of the predecessor cell
+  int* flen;                 // [nb][F] |frontier|
+  int* ccount;               // [nb][F] |cell| (table entries)
+  long long* mmin;           // [nb][F] smallest m of the frontier (LLONG_MAX if empty)
+  u64* trans;                // [nb][F] Σ |frontier_i| over comparable predecessors
+  u64* npairs;               // [nb][F] comparable predecessors (P)
   const long long* budgets;  // [nb] (clamped to 2*M(V))
   int IB;                    // parent-index bits in packed row keys
   int maximize;
@@ -212,10 +222,12 @@ struct remat_family_s {
   std::vector<long long> level_start;           // [n+2]
   std::vector<long long> level_maxR;            // [n+1]
   // DP state for up to nb_cap budgets
-  int nb_cap = 0;
-  remat::DevBuf<remat::Frontier> frontier;
-  remat::DevBuf<int> flen, ccount, npairs;
-  remat::DevBuf<long long> trans, budgets, results, partials;
+  int narrow = 0;                               // 32-bit row keys + 8 B entries
+  remat::DevBuf<unsigned char> fe;
+  remat::DevBuf<int> parent, flen, ccount;
+  remat::DevBuf<long long> mmin, budgets, results;
+  remat::DevBuf<u64> trans, npairs;
+  remat::DevBuf<unsigned> ctr;                  // per-tile chunk counters
   remat::DevBuf<u64> rowscratch, chain_out, cached_out;
   remat::DevBuf<long long> stage_out, terms;
   remat::DevBuf<int> chain_idx;

@@ -10,9 +10,8 @@
 //   cell i with m + fixed_ij <= B.
 // opt[j][t2] = lexicographic min over (m2, i) — the reference's strict `<`
 // push in family order keeps the first (smallest) i among equal m2.  The
-// reduction is a 64-bit atomicMin on the packed key (m2 << IB) | i in a
-// shared-memory row over t2 ∈ [0, T(L_j)], so it is order-independent and
-// deterministic.
+// reduction is an atomic min on the packed key (m2 << IB) | i in a dense row
+// over t2 ∈ [0, T(L_j)], so it is order-independent and deterministic.
 //
 // Pair constants from per-member prefix terms:
 //   fixed_ij = 2(M(L_j) − M(L_i)) + stage_base_j
@@ -22,312 +21,476 @@
 // the (small) boundary or Σ_c coef_c · popc(L_i ∩ ∂L_j ∩ class_c) over the
 // graph's weight classes, whichever is cheaper for this target.
 //
-// Finalisation (K5) turns the row into the compact frontier (strict prefix-min
-// of m in t-ascending order, t-descending for maximize; planner.py:153-161)
-// and records |cell|, |frontier| and Σ_i|frontier_i| over comparable i —
-// exactly table_entries, states_visited and transitions (Appendix A.3).
+// Work decomposition (k_relax_tile): a CTA owns a TILE of TJ consecutive
+// targets of one level (their rows live side by side in shared memory) and a
+// share of the predecessor range.  A warp tests 32 predecessors against all
+// TJ targets (lane = predecessor), turns the comparable (predecessor, target)
+// pairs into per-pair constants (lane = pair), then relaxes the flattened
+// (pair, frontier entry) items with its 32 lanes.  Pairs of one predecessor
+// are adjacent, so a frontier entry fetched for one target is an L1 hit for
+// the next: one L2 read of a predecessor's frontier feeds every comparable
+// target of the tile (SURVEY §7 hard part 2).  Frontier entries are stored
+// with m strictly decreasing, so the budget-feasible ones are a suffix and a
+// pair whose cap is below the frontier's smallest m is skipped outright.
+//
+// Finalisation (K5) turns each row into the compact frontier (strict
+// prefix-min of m in t-ascending order, t-descending for maximize;
+// planner.py:153-161), one warp per row, and records |cell| and |frontier|;
+// with Σ_i|frontier_i| and the comparable-pair counts accumulated during the
+// scan these are exactly table_entries, states_visited and transitions
+// (Appendix A.3).
 #include <algorithm>
+#include <climits>
 
 #include "device.cuh"
 
 namespace remat {
 
-// One queued predecessor of the current chunk (32 B -> two LDS.128).
-constexpr int kWarpMap = 512;  // items per round of a warp's item -> predecessor map
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxTJ = 32;   // targets per tile (one comparable bit each)
 
-struct __align__(16) QEntry {
-  long long foff;  // first frontier entry of the predecessor (budget-offset)
-  long long cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
-  long long dm;    // dm_ij
-  int dt;          // dt_ij (<= T(V) < 2^24)
-  int i;           // predecessor family index
+template <bool NARROW>
+struct Traits;
+template <>
+struct Traits<true> {
+  using Key = unsigned;
+  using E = EntryN;
+  static constexpr unsigned INF = 0xffffffffu;
+};
+template <>
+struct Traits<false> {
+  using Key = u64;
+  using E = EntryW;
+  static constexpr u64 INF = ~0ull;
 };
 
-// opt[t2] = min(opt[t2], key).  sm_100 has no native 64-bit shared-memory
-// min (it lowers to a CAS loop), so read first: a losing candidate issues no
-// atomic at all.  Global rows use the native ATOM.MIN.64.
-__device__ __forceinline__ void row_min(u64* row, long long t2, u64 key, bool smem) {
+// One relaxable (predecessor, target) pair of a warp's current group.
+struct __align__(16) PairQ {
+  long long base;  // entry index of item 0 of this pair, minus its item offset
+  long long cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
+  u64 kb;          // (dm_ij << IB) | i: key = (m << IB) + kb
+  int dtr;         // target row offset in the tile + dt_ij
+  int pad;
+};
+
+// Shared-memory carve-up of k_relax_tile (host and device agree on it).
+struct TileArgs {
+  long long jbase;  // first target of the level (= end of the predecessor range)
+  int width;        // targets in the level
+  int TJ;           // targets per tile
+  int splits;       // CTAs per tile (they share the tile's predecessor chunks)
+  int R;            // row stride (level max T(L)+1)
+  int smem_rows;    // rows in shared memory (else in grow)
+  int cls;          // weight-class path available
+  int rows_pb;      // rows per budget in grow (tiles · TJ)
+  void* grow;       // [nb][rows_pb][R] global rows (split / oversized levels)
+  unsigned* ctr;    // [nb][tiles] next predecessor chunk of the tile (zeroed per level)
+  int tiles;
+  int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_tacc, off_pairs, off_q, off_rows;
+  int bytes;
+};
+
+template <int W, bool NARROW>
+static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
+  using Key = typename Traits<NARROW>::Key;
+  TileArgs a{};
+  a.TJ = TJ;
+  a.R = R;
+  a.smem_rows = smem_rows;
+  a.cls = cls;
+  int o = 0;
+  auto take = [&](int bytes) {
+    int at = o;
+    o += (bytes + 15) & ~15;
+    return at;
+  };
+  a.off_tL = take(TJ * W * 8);
+  a.off_tB = take(TJ * W * 8);
+  a.off_tc = take(TJ * 4 * 8);
+  a.off_tcls = take(TJ * 4);
+  a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
+  a.off_tacc = take(TJ * 2 * 8);
+  a.off_pairs = take(kWarps * 32 * TJ * 2);
+  a.off_q = take(kWarps * 32 * (int)sizeof(PairQ));
+  a.off_rows = take(smem_rows ? TJ * R * (int)sizeof(Key) : 0);
+  a.bytes = o;
+  return a;
+}
+
+__device__ __forceinline__ void key_min(unsigned* p, unsigned key, bool) {
+  if (key < *p) atomicMin(p, key);
+}
+// sm_100 has no native 64-bit shared-memory min (it lowers to a CAS loop), so
+// read first: a losing candidate issues no atomic at all.  Global rows use the
+// native 64-bit atomic min.
+__device__ __forceinline__ void key_min(u64* p, u64 key, bool smem) {
   if (smem) {
-    u64 old = row[t2];
+    u64 old = *p;
     while (key < old) {
-      u64 prev = atomicCAS(row + t2, old, key);
+      u64 prev = atomicCAS(p, old, key);
       if (prev == old) break;
       old = prev;
     }
-  } else {
-    atomicMin(row + t2, key);
+  } else if (key < *p) {
+    atomicMin(p, key);
   }
 }
 
-// K5 on a finished row: |cell|, the strict prefix-min frontier in t order
-// (ascending for minimize, descending for maximize; planner.py:153-161),
+template <typename T>
+__device__ __forceinline__ T warp_min_all(T v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    T o = __shfl_xor_sync(kFull, v, m);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max_all(T v) {
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    T o = __shfl_xor_sync(kFull, v, m);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_min(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    T o = __shfl_up_sync(kFull, v, d);
+    if (lane >= d) v = o < v ? o : v;
+  }
+  return v;
+}
+
+// K5 for one finished row (one warp): |cell|, the strict prefix-min frontier in
+// t order (ascending for minimize, descending for maximize; planner.py:153-161)
 // compacted into the member's frontier slot with its back-pointers.
-__device__ void finalize_row(const u64* row, long long R, const DpView& dp, const FamilyView& fv,
-                             long long j, int b, long long trans_acc, long long pairs_acc,
-                             u64* scr) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+template <bool NARROW>
+__device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int Rj,
+                                  const DpView& dp, const FamilyView& fv, long long j, int b) {
+  using Key = typename Traits<NARROW>::Key;
+  using E = typename Traits<NARROW>::E;
+  constexpr Key INF = Traits<NARROW>::INF;
+  const int lane = threadIdx.x & 31;
   const long long F = fv.F;
   const int IB = dp.IB;
-  const int per = (int)((R + nt - 1) / nt);
-  const long long s0 = (long long)tid * per, s1 = min(R, s0 + per);
   const bool mx = dp.maximize;
-  u64 lmin = ~0ull;
-  unsigned cells = 0;
-  for (long long s = s0; s < s1; s++) {
-    u64 key = row[mx ? R - 1 - s : s];
-    if (key != ~0ull) {
+  const int per = (Rj + 31) / 32;
+  const int s0 = min(Rj, lane * per), s1 = min(Rj, s0 + per);
+  Key lmin = INF;
+  int cells = 0;
+  for (int s = s0; s < s1; s++) {
+    Key key = row[mx ? Rj - 1 - s : s];
+    if (key != INF) {
       cells++;
-      u64 m = key >> IB;
+      Key m = key >> IB;
       lmin = m < lmin ? m : lmin;
     }
   }
-  const u64 pm = block_exclusive_min(lmin, scr);
-  unsigned nf = 0;
-  u64 run = pm;
-  for (long long s = s0; s < s1; s++) {
-    u64 key = row[mx ? R - 1 - s : s];
-    if (key != ~0ull) {
-      u64 m = key >> IB;
-      if (m < run) {
-        nf++;
-        run = m;
-      }
+  Key incl = warp_incl_min(lmin);
+  Key pm = __shfl_up_sync(kFull, incl, 1);
+  if (lane == 0) pm = INF;
+  int nf = 0;
+  Key run = pm;
+  for (int s = s0; s < s1; s++) {
+    Key key = row[mx ? Rj - 1 - s : s];
+    if (key != INF && (key >> IB) < run) {
+      nf++;
+      run = key >> IB;
     }
   }
-  u64 tot2;
-  u64 ex2 = block_exclusive_sum<u64>(((u64)cells << 32) | nf, scr, &tot2);
-  Frontier* out = dp.frontier + (long long)b * dp.slots + fv.foff[j];
-  unsigned pos = (unsigned)(ex2 & 0xffffffffu);
+  const int nf_incl = warp_inclusive_sum(nf);
+  const int nf_tot = __shfl_sync(kFull, nf_incl, 31);
+  const int cells_tot = warp_sum(cells);
+  const long long slot0 = (long long)b * dp.slots + fv.foff[j];
+  E* out = reinterpret_cast<E*>(dp.fe) + slot0;
+  int* par = dp.parent + slot0;
+  int pos = nf_incl - nf;
   run = pm;
-  const u64 pmask = (1ull << IB) - 1;
-  for (long long s = s0; s < s1; s++) {
-    long long t = mx ? R - 1 - s : s;
-    u64 key = row[t];
-    if (key != ~0ull) {
-      u64 m = key >> IB;
-      if (m < run) {
-        Frontier f;
-        f.m = (long long)m;
-        f.t = (unsigned)t;
-        f.parent = (int)(key & pmask);
-        out[pos++] = f;
-        run = m;
-      }
+  const Key pmask = (Key(1) << IB) - 1;
+  for (int s = s0; s < s1; s++) {
+    const int t = mx ? Rj - 1 - s : s;
+    Key key = row[t];
+    if (key != INF && (key >> IB) < run) {
+      run = key >> IB;
+      E e{};
+      e.t = (unsigned)t;
+      e.m = run;
+      out[pos] = e;
+      par[pos] = (int)(key & pmask);
+      pos++;
     }
   }
-  if (tid == 0) {
-    dp.flen[(size_t)b * F + j] = (int)(tot2 & 0xffffffffu);
-    dp.ccount[(size_t)b * F + j] = (int)(tot2 >> 32);
-    dp.trans[(size_t)b * F + j] = trans_acc;
-    dp.npairs[(size_t)b * F + j] = (int)pairs_acc;
+  const Key gmin = __shfl_sync(kFull, incl, 31);
+  if (lane == 0) {
+    const size_t at = (size_t)b * F + j;
+    dp.flen[at] = nf_tot;
+    dp.ccount[at] = cells_tot;
+    dp.mmin[at] = nf_tot ? (long long)gmin : LLONG_MAX;
   }
 }
 
-// K4 (+K5 when unsplit).  Grid: (width·splits, nb); CTA (target tj, slice)
-// scans the predecessors [slice·P/splits, (slice+1)·P/splits) in 32-member
-// chunks.  Warps work independently (no block barrier in the main loop): a
-// warp tests 32 predecessors (lane = predecessor), queues the comparable ones
-// with a non-empty frontier in its private queue, stamps an item ->
-// predecessor map, and relaxes the flattened (predecessor, frontier entry)
-// items with its 32 lanes into the CTA's shared row.
-template <int W>
-__global__ void __launch_bounds__(kRelaxThreads)
-    k_relax_level(FamilyView fv, GraphView g, ClassView cv, DpView dp, long long jbase,
-                  long long pred_end, int splits, int smem_row, u64* grow, long long grow_stride,
-                  long long* part) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  __shared__ QEntry wq[kRelaxWarps][32];
-  __shared__ int wpre[kRelaxWarps][33];
-  __shared__ unsigned short wmap[kRelaxWarps][kWarpMap];
-  __shared__ u64 scr[33];
-  __shared__ long long red[2][kRelaxWarps];
-  __shared__ u64 bjc[2 * kMaxClasses * W];
-
+// K4 (+K5 when the tile is not split).  Grid: (tiles·splits, nb).
+template <int W, bool NARROW>
+__global__ void __launch_bounds__(kThreads)
+    k_relax_tile(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
+  using Key = typename Traits<NARROW>::Key;
+  using E = typename Traits<NARROW>::E;
+  constexpr Key INF = Traits<NARROW>::INF;
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int s_worked;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int TJ = ta.TJ, R = ta.R, splits = ta.splits;
+  if (tid == 0) s_worked = 0;
   const long long F = fv.F;
-  const int width = gridDim.x / splits;
-  const int tj = blockIdx.x / splits, slice = blockIdx.x - tj * splits;
-  const long long j = jbase + tj;
+  const int tile = blockIdx.x / splits;
   const int b = blockIdx.y;
-  u64* grow_j = grow ? grow + ((long long)b * width + tj) * grow_stride : nullptr;
-  u64* row = smem_row ? reinterpret_cast<u64*>(smraw) : grow_j;
+  const long long j0 = ta.jbase + (long long)tile * TJ;
+  const int ntj = (int)min((long long)TJ, ta.jbase + ta.width - j0);
 
-  u64 Lj[W], Bj[W];
-  int bcnt = 0;
-#pragma unroll
-  for (int w = 0; w < W; w++) {
-    Lj[w] = fv.masks[(size_t)w * F + j];
-    Bj[w] = fv.bound[(size_t)w * F + j];
-    bcnt += __popcll(Bj[w]);
+  u64* tL = reinterpret_cast<u64*>(sm + ta.off_tL);         // [TJ][W]
+  u64* tB = reinterpret_cast<u64*>(sm + ta.off_tB);         // [TJ][W]
+  long long* tc = reinterpret_cast<long long*>(sm + ta.off_tc);  // [TJ][4]
+  int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);     // [TJ]
+  u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
+  u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
+  unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
+  PairQ* wq = reinterpret_cast<PairQ*>(sm + ta.off_q) + warp * 32;
+  Key* grow_t = ta.grow ? reinterpret_cast<Key*>(ta.grow) +
+                              ((size_t)b * ta.rows_pb + (size_t)tile * TJ) * R
+                        : nullptr;
+  Key* rows = ta.smem_rows ? reinterpret_cast<Key*>(sm + ta.off_rows) : grow_t;
+  const bool srow = ta.smem_rows;
+
+  for (int e = tid; e < ntj * W; e += kThreads) {
+    const int jt = e / W, w = e - jt * W;
+    tL[e] = fv.masks[(size_t)w * F + j0 + jt];
+    tB[e] = fv.bound[(size_t)w * F + j0 + jt];
   }
-  const long long R = fv.TL[j] + 1;
-  const long long MLj = fv.ML[j], basej = fv.base[j], TLnbj = fv.TLnb[j], Mbj = fv.Mb[j];
+  for (int jt = tid; jt < ntj; jt += kThreads) {
+    const long long j = j0 + jt;
+    tc[jt * 4 + 0] = fv.ML[j];
+    tc[jt * 4 + 1] = fv.base[j];
+    tc[jt * 4 + 2] = fv.TLnb[j];
+    tc[jt * 4 + 3] = fv.Mb[j];
+    tacc[jt * 2] = 0;
+    tacc[jt * 2 + 1] = 0;
+  }
+  if (srow)
+    for (int t = tid; t < ntj * R; t += kThreads) rows[t] = INF;
+  __syncthreads();
+  const int KT = cv.KT, K = cv.KT + cv.KM;
+  if (ta.cls) {
+    for (int e = tid; e < ntj * K * W; e += kThreads) {
+      const int jt = e / (K * W), r = e - jt * K * W, c = r / W, w = r - c * W;
+      const u64 cls = c < KT ? cv.clsT[c * W + w] : cv.clsM[(c - KT) * W + w];
+      bjc[e] = tB[jt * W + w] & cls;
+    }
+  }
+  for (int jt = tid; jt < ntj; jt += kThreads) {
+    int bc = 0;
+    for (int w = 0; w < W; w++) bc += __popcll(tB[jt * W + w]);
+    tcls[jt] = ta.cls && K * W < bc;
+  }
+  __syncthreads();
+
   const long long B = dp.budgets[b];
   const int IB = dp.IB;
-  const int KT = cv.KT, K = cv.KT + cv.KM;
-  const bool use_cls = cv.enabled && K * W < bcnt;
-  if (use_cls) {
-    for (int e = tid; e < K * W; e += kRelaxThreads) {
-      int c = e / W, w = e - c * W;
-      u64 cls = c < KT ? cv.clsT[c * W + w] : cv.clsM[(c - KT) * W + w];
-      bjc[e] = fv.bound[(size_t)w * F + j] & cls;
-    }
-  }
-  if (smem_row)
-    for (long long t = tid; t < R; t += kRelaxThreads) row[t] = ~0ull;
-  __syncthreads();
-
-  const int* flen_b = dp.flen + (size_t)b * F;
   const long long fbase = (long long)b * dp.slots;
-  long long trans_acc = 0, pairs_acc = 0;
+  const int* flen_b = dp.flen + (size_t)b * F;
+  const long long* mmin_b = dp.mmin + (size_t)b * F;
+  const E* fe = reinterpret_cast<const E*>(dp.fe);
+  const long long pred_end = ta.jbase;
   const long long nch = (pred_end + 31) / 32;
-  const long long c0 = slice * nch / splits, c1 = (slice + 1) * nch / splits;
-  QEntry* q = wq[warp];
-  int* qpre = wpre[warp];
-  unsigned short* qmap = wmap[warp];
+  unsigned* ctr = ta.ctr + (size_t)b * ta.tiles + tile;
+  u64 my_trans = 0;  // lane jt accumulates target jt of the tile
+  u64 my_pairs = 0;
+  bool worked = false;
 
-  for (long long ch = c0 + warp; ch < c1; ch += kRelaxWarps) {
+  // Every CTA of the tile pulls 32-predecessor chunks from the tile's counter,
+  // so slices finish together and CTAs of a late wave find nothing left.
+  while (true) {
+    unsigned got = 0;
+    if (lane == 0) got = atomicAdd(ctr, 1u);
+    const long long ch = __shfl_sync(kFull, got, 0);
+    if (ch >= nch) break;
+    worked = true;
     const long long i = ch * 32 + lane;
+    unsigned mask = 0;
     int fl = 0;
-    bool comparable = false;
-    long long fixed = 0, dt = 0, dm = 0;
     if (i < pred_end) {
       u64 Li[W];
-      u64 acc = 0;
 #pragma unroll
-      for (int w = 0; w < W; w++) {
-        Li[w] = __ldg(fv.masks + (size_t)w * F + i);
-        acc |= Li[w] & ~Lj[w];
+      for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + i);
+      for (int jt = 0; jt < ntj; jt++) {
+        u64 acc = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
+        mask |= (acc == 0 ? 1u : 0u) << jt;
       }
-      comparable = acc == 0;
-      if (comparable) {
-        fl = flen_b[i];
-        if (fl > 0) {
-          long long ts = 0, ms = 0;
-          if (use_cls) {
-            for (int c = 0; c < K; c++) {
-              int pc = 0;
+      if (mask) fl = flen_b[i];
+    }
+    if (!__any_sync(kFull, mask)) continue;
+    for (int jt = 0; jt < ntj; jt++) {
+      const bool bit = (mask >> jt) & 1u;
+      const unsigned np = __popc(__ballot_sync(kFull, bit));
+      const unsigned tr = __reduce_add_sync(kFull, bit ? (unsigned)fl : 0u);
+      if (lane == jt) {
+        my_pairs += np;
+        my_trans += tr;
+      }
+    }
+    unsigned pm = fl > 0 ? mask : 0u;
+    const int cnt = __popc(pm);
+    const int cincl = warp_inclusive_sum(cnt);
+    const int npair = __shfl_sync(kFull, cincl, 31);
+    if (npair == 0) continue;
+    int pos = cincl - cnt;
+    while (pm) {
+      const int jt = __ffs(pm) - 1;
+      pm &= pm - 1;
+      wpairs[pos++] = (unsigned short)((lane << 5) | jt);
+    }
+    __syncwarp();
+    for (int g0 = 0; g0 < npair; g0 += 32) {
+      const int gk = min(32, npair - g0);
+      int c = 0;
+      PairQ q{};
+      if (lane < gk) {
+        const int pr = wpairs[g0 + lane];
+        const int jt = pr & 31;
+        const long long ii = ch * 32 + (pr >> 5);
+        u64 Li[W];
 #pragma unroll
-              for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bjc[c * W + w]);
-              if (c < KT) ts += __ldg(cv.coefT + c) * pc;
-              else ms += __ldg(cv.coefM + c - KT) * pc;
-            }
-          } else {
+        for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + ii);
+        long long ts = 0, ms = 0;
+        if (tcls[jt]) {
+          const u64* bj = bjc + (size_t)jt * K * W;
+          for (int cc = 0; cc < K; cc++) {
+            int pc = 0;
 #pragma unroll
-            for (int w = 0; w < W; w++) {
-              u64 x = Li[w] & Bj[w];
-              while (x) {
-                int v = w * 64 + __ffsll((long long)x) - 1;
-                x &= x - 1;
-                ts += __ldg(g.T + v);
-                ms += __ldg(g.M + v);
-              }
+            for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[cc * W + w]);
+            if (cc < KT) ts += __ldg(cv.coefT + cc) * pc;
+            else ms += __ldg(cv.coefM + cc - KT) * pc;
+          }
+        } else {
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            u64 x = Li[w] & tB[jt * W + w];
+            while (x) {
+              const int v = w * 64 + __ffsll((long long)x) - 1;
+              x &= x - 1;
+              ts += __ldg(g.T + v);
+              ms += __ldg(g.M + v);
             }
           }
-          fixed = 2 * (MLj - fv.ML[i]) + basej;
-          dt = TLnbj - fv.TL[i] + ts;
-          dm = Mbj - ms;
         }
+        const long long fixed = 2 * (tc[jt * 4 + 0] - __ldg(fv.ML + ii)) + tc[jt * 4 + 1];
+        const long long dt = tc[jt * 4 + 2] - __ldg(fv.TL + ii) + ts;
+        const long long dm = tc[jt * 4 + 3] - ms;
+        q.cap = B - fixed;
+        if (q.cap >= mmin_b[ii]) c = flen_b[ii];
+        q.base = fbase + __ldg(fv.foff + ii);
+        q.kb = ((u64)dm << IB) | (u64)ii;
+        q.dtr = jt * R + (int)dt;
       }
-    }
-    const unsigned has = __ballot_sync(kFull, fl > 0);
-    pairs_acc += __popc(__ballot_sync(kFull, comparable));
-    if (!has) continue;
-    const int qn = __popc(has);
-    const int incl = warp_inclusive_sum(fl);
-    const int total = __shfl_sync(kFull, incl, 31);
-    trans_acc += total;
-    if (fl > 0) {
-      const int qp = __popc(has & ((1u << lane) - 1));
-      QEntry e;
-      e.foff = fbase + fv.foff[i];
-      e.cap = B - fixed;
-      e.dm = dm;
-      e.dt = (int)dt;
-      e.i = (int)i;
-      q[qp] = e;
-      qpre[qp] = incl - fl;
-    }
-    if (lane == 0) qpre[qn] = total;
-    __syncwarp();
-    for (int r0 = 0; r0 < total; r0 += kWarpMap) {
-      const int r1 = min(total, r0 + kWarpMap);
-      if (lane < qn) {
-        const int a = max(qpre[lane], r0), z = min(qpre[lane + 1], r1);
-        for (int e = a; e < z; e++) qmap[e - r0] = (unsigned short)lane;
+      // compact the pairs with items (distinct, increasing start offsets)
+      const unsigned has = __ballot_sync(kFull, c > 0);
+      if (!has) continue;
+      const int iincl = warp_inclusive_sum(c);
+      const int tot = __shfl_sync(kFull, iincl, 31);
+      const unsigned lt = (1u << lane) - 1;
+      const int start = c > 0 ? iincl - c : INT_MAX;
+      if (c > 0) {
+        q.base -= iincl - c;
+        wq[__popc(has & lt)] = q;
       }
       __syncwarp();
-#pragma unroll 4
-      for (int e = r0 + lane; e < r1; e += 32) {
-        const int k = qmap[e - r0];
-        const QEntry qe = q[k];
-        const Frontier fr = dp.frontier[qe.foff + (e - qpre[k])];
-        if (fr.m <= qe.cap) {
-          u64 key = ((u64)(fr.m + qe.dm) << IB) | (u64)qe.i;
-          row_min(row, (long long)fr.t + qe.dt, key, smem_row);
+      // item e of the group belongs to the last compacted pair starting at or
+      // before e: per 32-item step, one REDUX.OR gathers the pair starts that
+      // fall inside the step and a popcount ranks each lane among them.
+      int kbase = -1;
+      for (int r = 0; r < tot; r += 32) {
+        const unsigned d = (unsigned)(start - r);
+        const unsigned smask = __reduce_or_sync(kFull, d < 32u ? 1u << d : 0u);
+        const int k = kbase + __popc(smask & (lt | (1u << lane)));
+        kbase += __popc(smask);
+        if (r + lane < tot) {
+          const PairQ& p = wq[k];
+          const E en = fe[p.base + r + lane];
+          if ((long long)en.m <= p.cap) {
+            const Key key = ((Key)en.m << IB) + (Key)p.kb;
+            key_min(rows + (en.t + p.dtr), key, srow);
+          }
         }
       }
       __syncwarp();
     }
   }
-  // per-CTA totals (trans_acc is warp-uniform; pairs_acc too)
-  if (lane == 0) {
-    red[0][warp] = trans_acc;
-    red[1][warp] = pairs_acc;
+  if (lane == 0 && worked) s_worked = 1;
+  if (lane < ntj && (my_pairs | my_trans)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + lane * 2), my_trans);
+    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + lane * 2 + 1), my_pairs);
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < kRelaxWarps; w++) {
-      trans_acc += red[0][w];
-      pairs_acc += red[1][w];
-    }
+  if (tid < ntj) {
+    const size_t at = (size_t)b * F + j0 + tid;
+    if (tacc[tid * 2]) atomicAdd(reinterpret_cast<unsigned long long*>(dp.trans + at), tacc[tid * 2]);
+    if (tacc[tid * 2 + 1])
+      atomicAdd(reinterpret_cast<unsigned long long*>(dp.npairs + at), tacc[tid * 2 + 1]);
   }
-  if (splits == 1 && smem_row) {
-    finalize_row(row, R, dp, fv, j, b, trans_acc, pairs_acc, scr);
+  if (splits == 1 && srow) {
+    for (int jt = warp; jt < ntj; jt += kWarps)
+      finalize_row_warp<NARROW>(rows + jt * R, (int)(fv.TL[j0 + jt] + 1), dp,
+                                fv, j0 + jt, b);
     return;
   }
-  if (smem_row)  // fold this slice's row into the target's global row
-    for (long long t = tid; t < R; t += kRelaxThreads) {
-      u64 key = row[t];
-      if (key != ~0ull) atomicMin(grow_j + t, key);
+  if (srow && s_worked)  // fold this CTA's rows into the tile's global rows
+    for (int t = tid; t < ntj * R; t += kThreads) {
+      const Key key = rows[t];
+      if (key != INF) atomicMin(grow_t + t, key);
     }
-  if (tid == 0) {
-    long long* pp = part + (((long long)b * width + tj) * splits + slice) * 2;
-    pp[0] = trans_acc;
-    pp[1] = pairs_acc;
-  }
 }
 
-// K5 for split / global-row levels: one CTA per (target, budget).
-__global__ void __launch_bounds__(kRelaxThreads)
-    k_finalize_level(FamilyView fv, DpView dp, long long jbase, int width, int splits,
-                     const u64* __restrict__ grow, long long grow_stride,
-                     const long long* __restrict__ part) {
-  __shared__ u64 scr[33];
-  const int tj = blockIdx.x, b = blockIdx.y;
+// K5 for split / global-row levels: one warp per (target, budget).
+template <bool NARROW>
+__global__ void __launch_bounds__(kThreads)
+    k_finalize_rows(FamilyView fv, DpView dp, long long jbase, int width, int rows_pb, int R,
+                    const void* __restrict__ grow) {
+  using Key = typename Traits<NARROW>::Key;
+  const int tj = blockIdx.x * kWarps + (threadIdx.x >> 5), b = blockIdx.y;
+  if (tj >= width) return;
   const long long j = jbase + tj;
-  long long tr = 0, pr = 0;
-  const long long* pp = part + ((long long)b * width + tj) * splits * 2;
-  for (int s = 0; s < splits; s++) {
-    tr += pp[2 * s];
-    pr += pp[2 * s + 1];
-  }
-  finalize_row(grow + ((long long)b * width + tj) * grow_stride, fv.TL[j] + 1, dp, fv, j, b, tr,
-               pr, scr);
+  const Key* row = reinterpret_cast<const Key*>(grow) + ((size_t)b * rows_pb + tj) * R;
+  finalize_row_warp<NARROW>(row, (int)(fv.TL[j] + 1), dp, fv, j, b);
 }
 
+template <typename Key>
+__global__ void k_fill(Key* p, size_t n, Key v) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+template <bool NARROW>
 __global__ void k_dp_init(DpView dp, long long F, int nb) {
+  using E = typename Traits<NARROW>::E;
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= nb) return;
-  Frontier f;
-  f.m = 0;
-  f.t = 0;
-  f.parent = -1;
-  dp.frontier[(long long)b * dp.slots] = f;  // foff[0] == 0: the empty set
+  E e{};
+  e.t = 0;
+  e.m = 0;
+  reinterpret_cast<E*>(dp.fe)[(long long)b * dp.slots] = e;  // foff[0] == 0: the empty set
+  dp.parent[(long long)b * dp.slots] = -1;
   dp.flen[(size_t)b * F] = 1;
   dp.ccount[(size_t)b * F] = 1;
-  dp.trans[(size_t)b * F] = 0;
-  dp.npairs[(size_t)b * F] = 0;
+  dp.mmin[(size_t)b * F] = 0;
 }
 
 // SearchStats, recomputed from the final table (Appendix A.3).
@@ -338,8 +501,8 @@ __global__ void k_dp_stats(DpView dp, long long F, long long* __restrict__ out) 
   for (long long i = threadIdx.x; i < F; i += blockDim.x) {
     sv += dp.flen[(size_t)b * F + i];
     te += dp.ccount[(size_t)b * F + i];
-    tr += dp.trans[(size_t)b * F + i];
-    np += dp.npairs[(size_t)b * F + i];
+    tr += (long long)dp.trans[(size_t)b * F + i];
+    np += (long long)dp.npairs[(size_t)b * F + i];
   }
   sv = warp_sum(sv);
   te = warp_sum(te);
@@ -372,23 +535,27 @@ __global__ void k_dp_stats(DpView dp, long long F, long long* __restrict__ out) 
 // finds that entry in the parent's frontier with a warp-wide ballot.
 // expect[b] = {t*, m_final, budget, 1}; klen[b] = k (0 when infeasible,
 // -1 on an inconsistent table).
-template <int W>
+template <int W, bool NARROW>
 __global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
                               int* __restrict__ path, u64* __restrict__ chain_out,
                               int* __restrict__ klen, long long* __restrict__ expect) {
+  using E = typename Traits<NARROW>::E;
   const int b = blockIdx.x, lane = threadIdx.x;
   const long long F = fv.F;
   const long long fbase = (long long)b * dp.slots;
+  const E* fe = reinterpret_cast<const E*>(dp.fe);
   int* pth = path + (size_t)b * (n + 2);
   long long j = F - 1;
   if (dp.flen[(size_t)b * F + j] == 0) {
     if (lane == 0) klen[b] = 0;
     return;
   }
-  Frontier cur = dp.frontier[fbase + fv.foff[j]];
+  long long at = fbase + fv.foff[j];
+  E cur = fe[at];
+  int cpar = dp.parent[at];
   if (lane == 0) {
     expect[b * 4 + 0] = cur.t;
-    expect[b * 4 + 1] = cur.m;
+    expect[b * 4 + 1] = (long long)cur.m;
     expect[b * 4 + 2] = dp.budgets[b];
     expect[b * 4 + 3] = 1;
   }
@@ -398,11 +565,11 @@ __global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
     if (lane == 0) pth[len] = (int)j;
     len++;
     if (j == 0) break;
-    if (len > n + 1 || cur.parent < 0) {
+    if (len > n + 1 || cpar < 0) {
       bad = true;
       break;
     }
-    const long long par = cur.parent;
+    const long long par = cpar;
     long long ts = 0;
     if (lane < W)
       ts = word_weight(fv.masks[(size_t)lane * F + par] & fv.bound[(size_t)lane * F + j], lane,
@@ -415,10 +582,12 @@ __global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
     bool found = false;
     for (int s0 = 0; s0 < nfp && !found; s0 += 32) {
       int s = s0 + lane;
-      bool hit = s < nfp && (long long)dp.frontier[pb + s].t == tp;
+      bool hit = s < nfp && (long long)fe[pb + s].t == tp;
       unsigned bal = __ballot_sync(kFull, hit);
       if (bal) {
-        cur = dp.frontier[pb + s0 + __ffs(bal) - 1];
+        const long long a2 = pb + s0 + __ffs(bal) - 1;
+        cur = fe[a2];
+        cpar = dp.parent[a2];
         found = true;
       }
     }
@@ -446,22 +615,26 @@ __global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
 // host driver
 // ---------------------------------------------------------------------------
 
-static constexpr int kSmemLimit = 200 * 1024;  // dynamic row bytes per CTA
+static constexpr int kSmemLimit = 200 * 1024;  // dynamic shared bytes per CTA
+static constexpr int kRowBudget = 64 * 1024;   // tile rows per CTA (4 CTAs/SM)
 
-template <int W>
+template <int W, bool NARROW>
 static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int objective,
                    remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                    long long* stage_memory) {
+  using Key = typename Traits<NARROW>::Key;
+  using E = typename Traits<NARROW>::E;
   remat_graph_s* g = f->g;
   cudaStream_t s = g->stream;
   const int nb = (int)budgets.size();
   const int n = g->n;
   const long long F = f->F;
   int rc;
-  if ((rc = f->frontier.ensure((size_t)nb * f->slots)) < 0 ||
+  if ((rc = f->fe.ensure((size_t)nb * f->slots * sizeof(E))) < 0 ||
+      (rc = f->parent.ensure((size_t)nb * f->slots)) < 0 ||
       (rc = f->flen.ensure((size_t)nb * F)) < 0 || (rc = f->ccount.ensure((size_t)nb * F)) < 0 ||
-      (rc = f->trans.ensure((size_t)nb * F)) < 0 || (rc = f->budgets.ensure(nb)) < 0 ||
-      (rc = f->npairs.ensure((size_t)nb * F)) < 0 ||
+      (rc = f->mmin.ensure((size_t)nb * F)) < 0 || (rc = f->trans.ensure((size_t)nb * F)) < 0 ||
+      (rc = f->npairs.ensure((size_t)nb * F)) < 0 || (rc = f->budgets.ensure(nb)) < 0 ||
       (rc = f->results.ensure((size_t)nb * 20)) < 0 ||
       (rc = f->chain_out.ensure((size_t)nb * (n + 1) * W)) < 0 ||
       (rc = f->cached_out.ensure((size_t)nb * (n + 1) * W)) < 0 ||
@@ -472,21 +645,24 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
     return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    RM_CUDA(cudaFuncSetAttribute(k_relax_level<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemLimit));
+    RM_CUDA(cudaFuncSetAttribute(k_relax_tile<W, NARROW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     attr_set = true;
   }
-  DpView dp{f->slots,    f->frontier.p, f->flen.p, f->ccount.p, f->trans.p,
-            f->npairs.p, f->budgets.p,  f->IB,     objective == REMAT_MAXIMIZE};
+  DpView dp{f->slots,  f->fe.p,   f->parent.p,  f->flen.p,    f->ccount.p, f->mmin.p,
+            f->trans.p, f->npairs.p, f->budgets.p, f->IB, objective == REMAT_MAXIMIZE};
   FamilyView fv = f->view();
   GraphView gv = g->view();
   ClassView cv = g->classes();
+  const int K = cv.KT + cv.KM;
   Events& ev = g->ev;
   const long long launches0 = remat_kernel_launch_count();
   RM_CUDA(cudaMemcpyAsync(f->budgets.p, budgets.data(), sizeof(long long) * nb,
                           cudaMemcpyHostToDevice, s));
   RM_CUDA(cudaEventRecord(ev.e[3], s));
-  k_dp_init<<<(nb + 127) / 128, 128, 0, s>>>(dp, F, nb);
+  RM_CUDA(cudaMemsetAsync(f->trans.p, 0, sizeof(u64) * nb * F, s));
+  RM_CUDA(cudaMemsetAsync(f->npairs.p, 0, sizeof(u64) * nb * F, s));
+  k_dp_init<NARROW><<<(nb + 127) / 128, 128, 0, s>>>(dp, F, nb);
   RM_LAUNCHED();
   long long relax_launches = 0;
   static int num_sms = 0;
@@ -495,31 +671,47 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   for (int lvl = 1; lvl <= n; lvl++) {
     const long long j0 = f->level_start[lvl], width = f->level_start[lvl + 1] - j0;
     if (width == 0) continue;
-    const long long R = f->level_maxR[lvl];
-    const bool in_smem = R * 8 <= kSmemLimit;
-    const long long nch = (j0 + kRelaxThreads - 1) / kRelaxThreads;
+    const int R = (int)f->level_maxR[lvl];
+    // targets per tile: as many rows as fit the per-CTA row budget, <= width
+    int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ / 2, width),
+                                      std::max<long long>(1, kRowBudget / ((long long)R * sizeof(Key))));
+    const long long nch = (j0 + 31) / 32;
+    // fewer targets per tile where the level is too small to give every
+    // resident warp a couple of (tile, chunk) tasks
+    const long long want = (long long)num_sms * 64;
+    while (TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
+    const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
+    TileArgs ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
+    if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
+    const long long tiles = (width + TJ - 1) / TJ;
     // split the predecessor scan across CTAs when the level alone cannot fill
     // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
-    long long splits = (target_ctas + width * nb - 1) / (width * nb);
-    splits = std::max(1LL, std::min(splits, nch / 2));
-    u64* grow = nullptr;
-    long long* part = nullptr;
-    if (splits > 1 || !in_smem) {
-      if ((rc = f->rowscratch.ensure((size_t)width * nb * R)) < 0 ||
-          (rc = f->partials.ensure((size_t)width * nb * splits * 2)) < 0)
-        return rc;
-      grow = f->rowscratch.p;
-      part = f->partials.p;
-      RM_CUDA(cudaMemsetAsync(grow, 0xff, sizeof(u64) * width * nb * R, s));
+    long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
+    splits = std::max(1LL, std::min(splits, nch / kWarps));
+    ta.jbase = j0;
+    ta.width = (int)width;
+    ta.splits = (int)splits;
+    ta.grow = nullptr;
+    ta.rows_pb = (int)(tiles * TJ);
+    ta.tiles = (int)tiles;
+    if ((rc = f->ctr.ensure((size_t)nb * tiles)) < 0) return rc;
+    ta.ctr = f->ctr.p;
+    RM_CUDA(cudaMemsetAsync(ta.ctr, 0, sizeof(unsigned) * nb * tiles, s));
+    if (splits > 1 || !ta.smem_rows) {
+      const size_t cells = (size_t)nb * tiles * TJ * R;
+      if ((rc = f->rowscratch.ensure((cells * sizeof(Key) + 7) / 8)) < 0) return rc;
+      ta.grow = f->rowscratch.p;
+      k_fill<Key><<<(unsigned)std::min<size_t>((cells + 255) / 256, 4096), 256, 0, s>>>(
+          reinterpret_cast<Key*>(ta.grow), cells, Traits<NARROW>::INF);
+      RM_LAUNCHED();
     }
-    k_relax_level<W><<<dim3((unsigned)(width * splits), (unsigned)nb), kRelaxThreads,
-                       in_smem ? (size_t)R * 8 : 0, s>>>(fv, gv, cv, dp, j0, j0, (int)splits,
-                                                         in_smem ? 1 : 0, grow, R, part);
+    k_relax_tile<W, NARROW><<<dim3((unsigned)(tiles * splits), (unsigned)nb), kThreads, ta.bytes,
+                              s>>>(fv, gv, cv, dp, ta);
     RM_LAUNCHED();
     relax_launches++;
-    if (grow) {
-      k_finalize_level<<<dim3((unsigned)width, (unsigned)nb), kRelaxThreads, 0, s>>>(
-          fv, dp, j0, (int)width, (int)splits, grow, R, part);
+    if (ta.grow) {
+      k_finalize_rows<NARROW><<<dim3((unsigned)((width + kWarps - 1) / kWarps), (unsigned)nb),
+                                kThreads, 0, s>>>(fv, dp, j0, (int)width, ta.rows_pb, R, ta.grow);
       RM_LAUNCHED();
     }
   }
@@ -528,7 +720,8 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   long long* stats = f->results.p + nb * 4;   // [nb][5]
   long long* evres = f->results.p + nb * 9;   // [nb][8]
   int* klen = f->chain_idx.p + (size_t)nb * (n + 2);
-  k_reconstruct<W><<<nb, 32, 0, s>>>(fv, gv, dp, n, f->chain_idx.p, f->chain_out.p, klen, expect);
+  k_reconstruct<W, NARROW><<<nb, 32, 0, s>>>(fv, gv, dp, n, f->chain_idx.p, f->chain_out.p, klen,
+                                             expect);
   RM_LAUNCHED();
   if ((rc = evaluate_chains(g, nb, f->chain_out.p, klen, expect, f->stage_out.p,
                             f->cached_out.p, evres, f->terms.p, f->stage_bound.p)) < 0)
@@ -602,7 +795,10 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
   int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
   dispatch_words(f->g->Wp, [&](auto wc) {
     constexpr int W = decltype(wc)::value;
-    rc = solve_w<W>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
+    if (f->narrow)
+      rc = solve_w<W, true>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
+    else
+      rc = solve_w<W, false>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
   });
   return rc;
 }
