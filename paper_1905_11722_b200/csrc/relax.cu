@@ -48,7 +48,29 @@ namespace remat {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kMaxTJ = 32;   // targets per tile (one comparable bit each)
+constexpr int kMaxTJ = 8;    // targets per tile (one comparable bit each, <= 32)
+
+// One relaxable (predecessor, target) pair of a warp's current group.
+struct __align__(16) PairQN {  // narrow: one LDS.128
+  int base;       // entry index (within the budget's table) of item 0, minus its item offset
+  unsigned cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
+  unsigned kb;    // (dm_ij << IB) | i: key = (m << IB) + kb
+  int dtr;        // target row offset in the tile + dt_ij
+};
+struct __align__(16) PairQW {
+  long long base;
+  long long cap;
+  u64 kb;
+  int dtr;
+  int pad;
+};
+
+// A live predecessor of a warp's chunk: its entries start at table index
+// base + (item offset), its budget-feasible pairs are wq[q0, q1).
+struct __align__(16) PredRec {
+  long long base;
+  int q0, q1;
+};
 
 template <bool NARROW>
 struct Traits;
@@ -56,22 +78,39 @@ template <>
 struct Traits<true> {
   using Key = unsigned;
   using E = EntryN;
+  using Q = PairQN;
+  using M = unsigned;
   static constexpr unsigned INF = 0xffffffffu;
+  // one LDG.64 per entry (entries of earlier levels are read-only while a
+  // level is relaxed, so the non-coherent path is safe)
+  static __device__ __forceinline__ void load(const E* p, unsigned& t, unsigned& m) {
+    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    t = v.x;
+    m = v.y;
+  }
+  static __device__ __forceinline__ PairQN lds(const PairQN* p) {  // one LDS.128
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    PairQN q;
+    q.base = (int)v.x;
+    q.cap = v.y;
+    q.kb = v.z;
+    q.dtr = (int)v.w;
+    return q;
+  }
 };
 template <>
 struct Traits<false> {
   using Key = u64;
   using E = EntryW;
+  using Q = PairQW;
+  using M = long long;
   static constexpr u64 INF = ~0ull;
-};
-
-// One relaxable (predecessor, target) pair of a warp's current group.
-struct __align__(16) PairQ {
-  long long base;  // entry index of item 0 of this pair, minus its item offset
-  long long cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
-  u64 kb;          // (dm_ij << IB) | i: key = (m << IB) + kb
-  int dtr;         // target row offset in the tile + dt_ij
-  int pad;
+  static __device__ __forceinline__ void load(const E* p, unsigned& t, long long& m) {
+    const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(p));
+    t = (unsigned)v.x;
+    m = v.y;
+  }
+  static __device__ __forceinline__ PairQW lds(const PairQW* p) { return *p; }
 };
 
 // Shared-memory carve-up of k_relax_tile (host and device agree on it).
@@ -87,7 +126,7 @@ struct TileArgs {
   void* grow;       // [nb][rows_pb][R] global rows (split / oversized levels)
   unsigned* ctr;    // [nb][tiles] next predecessor chunk of the tile (zeroed per level)
   int tiles;
-  int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_tacc, off_pairs, off_q, off_rows;
+  int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_tacc, off_pairs, off_q, off_qs, off_rows;
   int bytes;
 };
 
@@ -112,7 +151,8 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
   a.off_tacc = take(TJ * 2 * 8);
   a.off_pairs = take(kWarps * 32 * TJ * 2);
-  a.off_q = take(kWarps * 32 * (int)sizeof(PairQ));
+  a.off_q = take(kWarps * 32 * TJ * (int)sizeof(typename Traits<NARROW>::Q));
+  a.off_qs = take(kWarps * 32 * (16 + 4));
   a.off_rows = take(smem_rows ? TJ * R * (int)sizeof(Key) : 0);
   a.bytes = o;
   return a;
@@ -135,6 +175,22 @@ __device__ __forceinline__ void key_min(u64* p, u64 key, bool smem) {
   } else if (key < *p) {
     atomicMin(p, key);
   }
+}
+
+// One candidate into a shared-memory row: row[t2] = min(row[t2], key) if `ok`.
+// Every candidate's slot t2 = t + dt_ij <= T(L_j) is inside the row even when
+// the budget test fails, so the probe is unconditional and the update a
+// predicated RED (no branch, no reconvergence); only ~1 in 6 candidates
+// improves its slot.
+__device__ __forceinline__ void relax_smem(unsigned a, unsigned key, bool ok) {
+  asm volatile(
+      "{\n\t.reg .pred o, q;\n\t.reg .u32 c;\n\t"
+      "ld.shared.u32 c, [%0];\n\t"
+      "setp.ne.u32 o, %2, 0;\n\t"
+      "setp.lt.and.u32 q, %1, c, o;\n\t"
+      "@q red.shared.min.u32 [%0], %1;\n\t}"
+      ::"r"(a), "r"(key), "r"((unsigned)ok)
+      : "memory");
 }
 
 template <typename T>
@@ -242,10 +298,13 @@ __global__ void __launch_bounds__(kThreads)
     k_relax_tile(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
   using Key = typename Traits<NARROW>::Key;
   using E = typename Traits<NARROW>::E;
+  using Q = typename Traits<NARROW>::Q;
+  using MT = typename Traits<NARROW>::M;
   constexpr Key INF = Traits<NARROW>::INF;
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int s_worked;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1;
   const int TJ = ta.TJ, R = ta.R, splits = ta.splits;
   if (tid == 0) s_worked = 0;
   const long long F = fv.F;
@@ -261,7 +320,9 @@ __global__ void __launch_bounds__(kThreads)
   u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
   u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
   unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
-  PairQ* wq = reinterpret_cast<PairQ*>(sm + ta.off_q) + warp * 32;
+  Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * 32 * TJ;  // feasible pairs of a chunk
+  PredRec* wrec = reinterpret_cast<PredRec*>(sm + ta.off_qs) + warp * 32;  // live predecessors
+  int* wpc = reinterpret_cast<int*>(sm + ta.off_qs + kWarps * 32 * 16) + warp * 32;
   Key* grow_t = ta.grow ? reinterpret_cast<Key*>(ta.grow) +
                               ((size_t)b * ta.rows_pb + (size_t)tile * TJ) * R
                         : nullptr;
@@ -346,26 +407,33 @@ __global__ void __launch_bounds__(kThreads)
         my_trans += tr;
       }
     }
+    // pairs (predecessor lane, target) in predecessor-major order
     unsigned pm = fl > 0 ? mask : 0u;
     const int cnt = __popc(pm);
     const int cincl = warp_inclusive_sum(cnt);
     const int npair = __shfl_sync(kFull, cincl, 31);
     if (npair == 0) continue;
-    int pos = cincl - cnt;
-    while (pm) {
-      const int jt = __ffs(pm) - 1;
-      pm &= pm - 1;
-      wpairs[pos++] = (unsigned short)((lane << 5) | jt);
+    {
+      int pos = cincl - cnt;
+      while (pm) {
+        const int jt = __ffs(pm) - 1;
+        pm &= pm - 1;
+        wpairs[pos++] = (unsigned short)((lane << 5) | jt);
+      }
     }
+    wpc[lane] = 0;
     __syncwarp();
+    // pair constants (lane = pair); budget-feasible pairs are kept, in order
+    int qn = 0;
     for (int g0 = 0; g0 < npair; g0 += 32) {
-      const int gk = min(32, npair - g0);
-      int c = 0;
-      PairQ q{};
-      if (lane < gk) {
+      bool ok = false;
+      Q q{};
+      int pl = 0;
+      if (lane < npair - g0) {
         const int pr = wpairs[g0 + lane];
         const int jt = pr & 31;
-        const long long ii = ch * 32 + (pr >> 5);
+        pl = pr >> 5;
+        const long long ii = ch * 32 + pl;
         u64 Li[W];
 #pragma unroll
         for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + ii);
@@ -394,44 +462,79 @@ __global__ void __launch_bounds__(kThreads)
         const long long fixed = 2 * (tc[jt * 4 + 0] - __ldg(fv.ML + ii)) + tc[jt * 4 + 1];
         const long long dt = tc[jt * 4 + 2] - __ldg(fv.TL + ii) + ts;
         const long long dm = tc[jt * 4 + 3] - ms;
-        q.cap = B - fixed;
-        if (q.cap >= mmin_b[ii]) c = flen_b[ii];
-        q.base = fbase + __ldg(fv.foff + ii);
-        q.kb = ((u64)dm << IB) | (u64)ii;
+        const long long cap = B - fixed;
+        ok = cap >= mmin_b[ii];
+        q.cap = (MT)max(cap, 0LL);
+        q.base = 0;
+        q.kb = (Key)(((u64)dm << IB) | (u64)ii);
         q.dtr = jt * R + (int)dt;
       }
-      // compact the pairs with items (distinct, increasing start offsets)
-      const unsigned has = __ballot_sync(kFull, c > 0);
-      if (!has) continue;
-      const int iincl = warp_inclusive_sum(c);
-      const int tot = __shfl_sync(kFull, iincl, 31);
-      const unsigned lt = (1u << lane) - 1;
-      const int start = c > 0 ? iincl - c : INT_MAX;
-      if (c > 0) {
-        q.base -= iincl - c;
-        wq[__popc(has & lt)] = q;
+      const unsigned okm = __ballot_sync(kFull, ok);
+      if (ok) {
+        wq[qn + __popc(okm & lt)] = q;
+        atomicAdd(wpc + pl, 1);
       }
-      __syncwarp();
-      // item e of the group belongs to the last compacted pair starting at or
-      // before e: per 32-item step, one REDUX.OR gathers the pair starts that
-      // fall inside the step and a popcount ranks each lane among them.
+      qn += __popc(okm);
+    }
+    __syncwarp();
+    // items = (predecessor, frontier entry), lane = predecessor again
+    const int pc = wpc[lane];
+    const int c = pc > 0 ? fl : 0;
+    const unsigned has = __ballot_sync(kFull, c > 0);
+    if (!has) continue;
+    const int pincl = warp_inclusive_sum(pc);
+    const int iincl = warp_inclusive_sum(c);
+    const int tot = __shfl_sync(kFull, iincl, 31);
+    const int start = c > 0 ? iincl - c : INT_MAX;
+    if (c > 0) {
+      PredRec rc;
+      rc.base = fbase + __ldg(fv.foff + i) - (iincl - c);
+      rc.q0 = pincl - pc;
+      rc.q1 = pincl;
+      wrec[__popc(has & lt)] = rc;
+    }
+    __syncwarp();
+    // Item e belongs to the last live predecessor starting at or before e:
+    // per 32-item step one REDUX.OR gathers the predecessor starts inside the
+    // step and a popcount ranks each lane among them.  One entry load then
+    // feeds every budget-feasible target of that predecessor in the tile
+    // (rows are addressed through the shared window directly when they live
+    // in shared memory, so the row probe is an LDS and the update an ATOMS).
+    const unsigned le = lt | (1u << lane);
+    // smem: rows addressed as 32-bit shared-window offsets; global: pointers
+    auto relax_items = [&](Key* __restrict__ rw, const unsigned rs, const bool smem) {
       int kbase = -1;
       for (int r = 0; r < tot; r += 32) {
         const unsigned d = (unsigned)(start - r);
         const unsigned smask = __reduce_or_sync(kFull, d < 32u ? 1u << d : 0u);
-        const int k = kbase + __popc(smask & (lt | (1u << lane)));
+        const int k = kbase + __popc(smask & le);
         kbase += __popc(smask);
         if (r + lane < tot) {
-          const PairQ& p = wq[k];
-          const E en = fe[p.base + r + lane];
-          if ((long long)en.m <= p.cap) {
-            const Key key = ((Key)en.m << IB) + (Key)p.kb;
-            key_min(rows + (en.t + p.dtr), key, srow);
+          const PredRec rec = wrec[k];
+          unsigned t;
+          MT m;
+          Traits<NARROW>::load(fe + (rec.base + r + lane), t, m);
+          const Key mk = (Key)m << IB;
+          const Q* qe = wq + rec.q1;
+          for (const Q* qp = wq + rec.q0; qp < qe; ++qp) {
+            const Q p = Traits<NARROW>::lds(qp);
+            if constexpr (NARROW) {
+              if (smem) {
+                relax_smem(rs + 4u * (t + (unsigned)p.dtr), mk + p.kb, m <= p.cap);
+                continue;
+              }
+            }
+            if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
           }
         }
       }
-      __syncwarp();
-    }
+    };
+    if (srow)
+      relax_items(reinterpret_cast<Key*>(sm + ta.off_rows),
+                  (unsigned)__cvta_generic_to_shared(sm + ta.off_rows), true);
+    else
+      relax_items(grow_t, 0u, false);
+    __syncwarp();
   }
   if (lane == 0 && worked) s_worked = 1;
   if (lane < ntj && (my_pairs | my_trans)) {
@@ -673,7 +776,7 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
     if (width == 0) continue;
     const int R = (int)f->level_maxR[lvl];
     // targets per tile: as many rows as fit the per-CTA row budget, <= width
-    int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ / 2, width),
+    int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ, width),
                                       std::max<long long>(1, kRowBudget / ((long long)R * sizeof(Key))));
     const long long nch = (j0 + 31) / 32;
     // fewer targets per tile where the level is too small to give every
@@ -795,7 +898,8 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
   int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
   dispatch_words(f->g->Wp, [&](auto wc) {
     constexpr int W = decltype(wc)::value;
-    if (f->narrow)
+    // narrow pair records hold entry offsets within one budget's table as int32
+    if (f->narrow && f->slots < (1LL << 31))
       rc = solve_w<W, true>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
     else
       rc = solve_w<W, false>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
