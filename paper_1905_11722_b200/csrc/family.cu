@@ -10,6 +10,8 @@
 // the largest-index maximal element of L ∪ {v}.  Every lower set is emitted
 // exactly once, so no hash/dedup is needed; each level is then ranked by mask
 // value, which reproduces the reference order (popcount, mask).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -422,58 +424,141 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 // host drivers
 // ---------------------------------------------------------------------------
 
+// K1 as ONE cooperative launch with one grid barrier per level (SURVEY §7
+// hard part 5: n = 516 dependent levels at C5).  Level k's members sit
+// UNSORTED in a ping-pong buffer U_k (with their maximal-element sets); in
+// the step for level k every warp emits canonical children of (member, 32-node
+// chunk) tasks into U_{k+1} at atomically reserved positions, while the same
+// step rank-sorts U_k into the family at ls[k] — both only read U_k, and the
+// emission order is irrelevant because U_{k+1} is ranked in the next step.
+//   ctr[k]    |level k| (ctr[0] = 1: the empty set, pre-set by the host)
+//   status[0] 1 when the lattice exceeds `cap` (LatticeTooLargeError)
+template <int W>
+__global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds, int n,
+                                                  long long cap, u64* __restrict__ fam,
+                                                  u64* __restrict__ U0, u64* __restrict__ U1,
+                                                  long long* __restrict__ ctr,
+                                                  long long* __restrict__ ls,
+                                                  int* __restrict__ status) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ u64 tile[256 * W];
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (long long)gridDim.x * 8;
+  const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int nch = (n + 31) / 32;
+  long long base = 0;  // ls[k]
+  for (int k = 0; k <= n; k++) {
+    const long long N = *((volatile long long*)(ctr + k));
+    if (base + N > cap) {  // uniform: every block read the same counters
+      if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = 1;
+      return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ls[k] = base;
+    const u64* cur = (k & 1) ? U1 : U0;  // [N][2W]: mask, maximal elements
+    u64* nxt = (k & 1) ? U0 : U1;
+    const long long room = cap - base - N;  // children that still fit under the cap
+    // (a) canonical children of level k
+    if (k < n)
+      for (long long task = gw; task < N * nch; task += nwarps) {
+        const long long p = task / nch;
+        const int v = (int)(task - p * nch) * 32 + lane;
+        u64 L[W], X[W], cx[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          L[w] = cur[p * 2 * W + w];
+          X[w] = cur[p * 2 * W + W + w];
+        }
+        const bool ok = v < n && canonical_child<W>(L, X, v, preds, cx);
+        const unsigned bal = __ballot_sync(kFull, ok);
+        if (!bal) continue;
+        unsigned long long at0 = 0;
+        if (lane == 0) at0 = atomicAdd(reinterpret_cast<unsigned long long*>(ctr + k + 1), (unsigned long long)__popc(bal));
+        at0 = __shfl_sync(kFull, at0, 0);
+        const long long at = (long long)at0 + __popc(bal & ((1u << lane) - 1));
+        if (ok && at < room) {
+#pragma unroll
+          for (int w = 0; w < W; w++) {
+            nxt[at * 2 * W + w] = L[w] | ((w == (v >> 6)) ? (1ull << (v & 63)) : 0ull);
+            nxt[at * 2 * W + W + w] = cx[w];
+          }
+        }
+      }
+    // (b) rank-sort level k by mask value: rank(i) = #{q : mask_q < mask_i}
+    for (long long i0 = (long long)blockIdx.x * 256; i0 < N; i0 += (long long)gridDim.x * 256) {
+      const long long i = i0 + threadIdx.x;
+      u64 me[W];
+#pragma unroll
+      for (int w = 0; w < W; w++) me[w] = i < N ? cur[i * 2 * W + w] : 0ull;
+      long long rank = 0;
+      for (long long t0 = 0; t0 < N; t0 += 256) {
+        const long long c = min(256LL, N - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < c * W; e += 256) {
+          const long long q = e / W;
+          tile[e] = cur[(t0 + q) * 2 * W + (e - q * W)];
+        }
+        __syncthreads();
+        if (i < N)
+          for (int q = 0; q < c; q++) rank += mask_less<W>(tile + q * W, me);
+      }
+      if (i < N)
+#pragma unroll
+        for (int w = 0; w < W; w++) fam[(base + rank) * W + w] = me[w];
+    }
+    base += N;
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ls[n + 1] = base;
+}
+
 template <int W>
 static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
                           std::vector<long long>& level_start) {
   cudaStream_t s = g->stream;
   const int n = g->n;
-  long long Fcap = std::max<long long>(1024, std::min<long long>(cap, 1 << 16));
-  int rc = fam.ensure((size_t)Fcap * W);
-  if (rc < 0) return rc;
-  DevBuf<u64> maxc, maxn, nrows, nmax;
-  DevBuf<long long> counts, offs;
-  if ((rc = maxc.ensure(W)) < 0) return rc;
-  RM_CUDA(cudaMemsetAsync(fam.p, 0, sizeof(u64) * W, s));
-  RM_CUDA(cudaMemsetAsync(maxc.p, 0, sizeof(u64) * W, s));
-  level_start.assign(1, 0);
-  long long width = 1, F = 1;
-  for (int lvl = 0; lvl < n; lvl++) {
-    const u64* cur = fam.p + (size_t)level_start.back() * W;
-    if ((rc = counts.ensure(width)) < 0 || (rc = offs.ensure(width)) < 0) return rc;
-    unsigned blocks = (unsigned)((width + 7) / 8);
-    k_enum_count<W><<<blocks, 256, 0, s>>>(cur, maxc.p, width, g->preds.p, n, counts.p);
-    RM_LAUNCHED();
-    long long next = 0;
-    if ((rc = scan_exclusive(counts.p, offs.p, width, s, &next)) < 0) return rc;
-    if (F + next > cap)
-      return fail(REMAT_ERR_LATTICE, "lattice too large: more than " + std::to_string(cap) +
-                                         " lower sets; raise the cap or use the pruned family");
-    if ((rc = nrows.ensure((size_t)next * W)) < 0 || (rc = nmax.ensure((size_t)next * W)) < 0)
-      return rc;
-    k_enum_emit<W><<<blocks, 256, 0, s>>>(cur, maxc.p, width, g->preds.p, n, offs.p, nrows.p,
-                                          nmax.p);
-    RM_LAUNCHED();
-    if (F + next > Fcap) {
-      long long nc = Fcap;
-      while (nc < F + next) nc *= 2;
-      DevBuf<u64> grown;
-      if ((rc = grown.ensure((size_t)nc * W)) < 0) return rc;
-      RM_CUDA(cudaMemcpyAsync(grown.p, fam.p, sizeof(u64) * W * F, cudaMemcpyDeviceToDevice, s));
-      std::swap(grown.p, fam.p);
-      std::swap(grown.n, fam.n);
-      Fcap = nc;
-    }
-    level_start.push_back(F);
-    if ((rc = maxn.ensure((size_t)next * W)) < 0) return rc;
-    k_rank_level<W><<<(unsigned)((next + 255) / 256), 256, 0, s>>>(
-        nrows.p, nmax.p, next, fam.p + (size_t)F * W, maxn.p);
-    RM_LAUNCHED();
-    std::swap(maxc.p, maxn.p);
-    std::swap(maxc.n, maxn.n);
-    F += next;
-    width = next;
+  // sized for the cap (a larger lattice raises LatticeTooLargeError):
+  // family cap x 8W bytes plus two level buffers of cap x 16W bytes in HBM
+  const long long Fcap = std::max<long long>(cap, n + 1);
+  int rc;
+  DevBuf<u64> U0, U1;
+  DevBuf<int> status;
+  DevBuf<long long> ctr, ls;
+  static int blocks_per_sm[17] = {}, num_sms = 0;
+  if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  if (!blocks_per_sm[W]) {
+    RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[W], k_enum_all<W>, 256, 0));
+    blocks_per_sm[W] = std::max(1, std::min(blocks_per_sm[W], 4));
   }
-  level_start.push_back(F);
+  const int nblk = num_sms * blocks_per_sm[W];
+  if ((rc = fam.ensure((size_t)Fcap * W)) < 0 || (rc = U0.ensure((size_t)Fcap * 2 * W)) < 0 ||
+      (rc = U1.ensure((size_t)Fcap * 2 * W)) < 0 || (rc = ctr.ensure(n + 2)) < 0 ||
+      (rc = ls.ensure(n + 2)) < 0 || (rc = status.ensure(1)) < 0)
+    return rc;
+  RM_CUDA(cudaMemsetAsync(U0.p, 0, sizeof(u64) * 2 * W, s));  // the empty set, no maximal elements
+  RM_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(long long) * (n + 2), s));
+  RM_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+  const long long one = 1;
+  RM_CUDA(cudaMemcpyAsync(ctr.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
+  const u64* preds = g->preds.p;
+  u64 *a0 = fam.p, *a1 = U0.p, *a2 = U1.p;
+  long long *a3 = ctr.p, *a4 = ls.p;
+  int* a5 = status.p;
+  int nn = n;
+  long long cp = cap;
+  void* args[] = {(void*)&preds, &nn, &cp, &a0, &a1, &a2, &a3, &a4, &a5};
+  RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_enum_all<W>, dim3(nblk), dim3(256), args, 0,
+                                      s));
+  RM_LAUNCHED();
+  int st = 0;
+  level_start.assign(n + 2, 0);
+  RM_CUDA(cudaMemcpyAsync(&st, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaMemcpyAsync(level_start.data(), ls.p, sizeof(long long) * (n + 2),
+                          cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  if (st)
+    return fail(REMAT_ERR_LATTICE, "lattice too large: more than " + std::to_string(cap) +
+                                       " lower sets; raise the cap or use the pruned family");
   return REMAT_OK;
 }
 
