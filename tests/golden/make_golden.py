@@ -8,7 +8,8 @@ Run in the build container only (it imports the read-only reference package at
 Every fixture stores the graph as the reference's own ``graph_to_document``
 (index order) plus the reference's outputs for it.  Node sets are written as
 hex strings.  ``--slow`` adds the named-shape cases whose reference solve takes
-minutes (C3 DenseNet-161, C5 random-dag n=516 p=0.5).
+minutes (C3 DenseNet-161, C5 random-dag n=516 p=0.5); ``--xslow`` writes
+named_xslow.json (C5 p=0.4, memory-centric U-Net; ~10 min).
 
 Fixtures (all keyed on reference call sites, file:line under pkg/src/remat):
   dp_corpus.json     dp_plan (planner.py:214) on seeded random DAGs, both
@@ -310,6 +311,29 @@ def named(slow: bool):
     return out
 
 
+def named_xslow():
+    """Reference runs that take many minutes in the build container: C5 at
+    p=0.4 (F=3,293, ~440 s of TransitionIndex) and memory-centric U-Net."""
+    out = []
+    g = generate(TopologySpec("random-dag", 516, seed=0, edge_prob=0.4))
+    rec = {"name": "random-dag", "kw": {"depth": 516, "seed": 0, "edge_prob": 0.4},
+           "graph": graph_to_document(g), "runs": []}
+    t0 = time.perf_counter()
+    b = 2 * g.total_memory
+    rec["runs"].append({"kind": "dp", "plan": plan_json(dp_plan(PlanRequest(g, b, "full"))),
+                        "ref_seconds": round(time.perf_counter() - t0, 3)})
+    print(f"  C5 p=0.4: {rec['runs'][-1]['ref_seconds']}s", flush=True)
+    out.append(rec)
+    g = graph_from_document(ours.unet_document(2))
+    rec = {"name": "unet", "kw": {"skip_len": 2}, "graph": graph_to_document(g), "runs": []}
+    t0 = time.perf_counter()
+    rec["runs"].append({"kind": "mc", "family": "full",
+                        "plan": plan_json(memory_centric_plan(g, "full")),
+                        "ref_seconds": round(time.perf_counter() - t0, 3)})
+    out.append(rec)
+    return out
+
+
 def dump(name: str, obj) -> None:
     path = OUT / name
     path.write_text(json.dumps(obj, separators=(",", ":")) + "\n")
@@ -327,6 +351,8 @@ def main() -> None:
         "reports.json": reports,
         "named.json": lambda: named(slow),
     }
+    if "--xslow" in sys.argv:
+        jobs = {"named_xslow.json": named_xslow}
     for fname, fn in jobs.items():
         if only and fname not in only:
             continue
