@@ -45,6 +45,9 @@ enum remat_objective { REMAT_MINIMIZE = 0, REMAT_MAXIMIZE = 1 };
 
 typedef struct remat_graph_s *remat_graph_t;   /* device-resident DAG          */
 typedef struct remat_family_s *remat_family_t; /* lower-set family + precompute */
+typedef struct remat_comm_s *remat_comm_t;     /* NCCL communicator (level sharding) */
+
+#define REMAT_COMM_ID_BYTES 128                /* sizeof(ncclUniqueId)        */
 
 typedef struct {
   int64_t states_visited, table_entries, transitions, dominated_skipped;
@@ -127,6 +130,38 @@ REMAT_API int remat_evaluate(remat_graph_t g, int32_t k, const uint64_t *chain,
  * traces: [total] live memory after each instruction, or NULL. */
 REMAT_API int remat_simulate(remat_graph_t g, int32_t nsched, const int64_t *offsets,
                    const int32_t *ops, remat_sim_info *info, int64_t *traces);
+
+/* ---- level sharding across GPUs (no reference counterpart:
+ * the reference is single-threaded) ----------------------
+ * The targets of every level of an exact-DP solve are split into contiguous
+ * rank ranges; after each level the ranks all-gather the finished frontiers
+ * (one ncclAllGather over NVLink).  Every rank ends with the whole table and
+ * returns the same plan as remat_solve on one GPU.  NCCL is loaded at run
+ * time (libnccl.so.2). */
+REMAT_API int remat_comm_unique_id(uint8_t *id /* [REMAT_COMM_ID_BYTES] */);
+REMAT_API int remat_comm_create(const uint8_t *id, int32_t world, int32_t rank,
+                                int32_t device, remat_comm_t *out);
+REMAT_API int remat_comm_free(remat_comm_t c);
+/* targets [begin, end) of a level [level_start, level_start + width) owned by
+ * `rank` (host-only helper, no device needed) */
+REMAT_API int remat_level_partition(int64_t level_start, int64_t width, int32_t world,
+                                    int32_t rank, int64_t *begin, int64_t *end);
+/* remat_solve with the level loop sharded over the communicator's ranks; every
+ * rank passes an identical family (same graph, same kind and cap). */
+REMAT_API int remat_solve_level_sharded(remat_family_t f, remat_comm_t c,
+                                        const int64_t *budgets, int32_t nb,
+                                        int32_t objective, remat_plan_info *info,
+                                        uint64_t *chain_masks, uint64_t *cached_masks,
+                                        int64_t *stage_memory);
+/* the same exchange with `world` replicas on ONE device (device copies in
+ * place of the all-gather): the single-GPU test form of level sharding.  The
+ * replicas must be families of one graph handle. */
+REMAT_API int remat_solve_level_sharded_loopback(remat_family_t *fams, int32_t world,
+                                                 const int64_t *budgets, int32_t nb,
+                                                 int32_t objective, remat_plan_info *info,
+                                                 uint64_t *chain_masks,
+                                                 uint64_t *cached_masks,
+                                                 int64_t *stage_memory);
 
 #ifdef __cplusplus
 }

@@ -100,6 +100,12 @@ def lib():
             "remat_evaluate": [_P, _I32, _P, C.POINTER(_I64), _P, C.POINTER(_I64),
                                C.POINTER(_I64), _P],
             "remat_simulate": [_P, _I32, _P, _P, _P, _P],
+            "remat_comm_unique_id": [_P],
+            "remat_comm_create": [_P, _I32, _I32, _I32, C.POINTER(_P)],
+            "remat_comm_free": [_P],
+            "remat_level_partition": [_I64, _I64, _I32, _I32, C.POINTER(_I64), C.POINTER(_I64)],
+            "remat_solve_level_sharded": [_P, _P, _P, _I32, _I32, _P, _P, _P, _P],
+            "remat_solve_level_sharded_loopback": [_P, _I32, _P, _I32, _I32, _P, _P, _P, _P],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -116,6 +122,8 @@ def exported_symbols() -> list[str]:
         "remat_graph_stream", "remat_family_create", "remat_family_size",
         "remat_family_masks", "remat_family_free", "remat_family_timings", "remat_solve",
         "remat_min_feasible_budget", "remat_evaluate", "remat_simulate",
+        "remat_comm_unique_id", "remat_comm_create", "remat_comm_free", "remat_level_partition",
+        "remat_solve_level_sharded", "remat_solve_level_sharded_loopback",
     ]
 
 
@@ -229,6 +237,51 @@ class DeviceGraph:
         return infos, offs, trace
 
 
+class Comm:
+    """An NCCL communicator inside libremat_b200 (level sharding)."""
+
+    ID_BYTES = 128
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * Comm.ID_BYTES)()
+        check(lib().remat_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, world: int, rank: int, device: int):
+        buf = (C.c_uint8 * Comm.ID_BYTES).from_buffer_copy(uid)
+        h = _P()
+        check(lib().remat_comm_create(buf, world, rank, device, C.byref(h)))
+        self.handle, self.world, self.rank, self.device = h, world, rank, device
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().remat_comm_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def level_partition(level_start: int, width: int, world: int, rank: int) -> tuple[int, int]:
+    """Targets [begin, end) of a level owned by ``rank`` (host-only)."""
+    a, b = _I64(), _I64()
+    check(lib().remat_level_partition(level_start, width, world, rank, C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def solve_loopback(fams: list["DeviceFamily"], budgets: list[int], objective: str):
+    """Level-sharded solve with ``len(fams)`` replicas on one device."""
+    arr = (_P * len(fams))(*[f.handle for f in fams])
+    f0 = fams[0]
+    return f0._solve_with(
+        lambda *a: lib().remat_solve_level_sharded_loopback(arr, len(fams), *a), budgets,
+        objective)
+
+
 def words_to_int(row) -> int:
     out = 0
     for k, x in enumerate(row):
@@ -290,6 +343,21 @@ class DeviceFamily:
                                 C.addressof(infos), chain.ctypes.data, cached.ctypes.data,
                                 stage.ctypes.data))
         return [self._unpack(infos[i], chain[i], cached[i], stage[i]) for i in range(nb)]
+
+    def _solve_with(self, fn, budgets: list[int], objective: str):
+        nb = len(budgets)
+        b = np.asarray([min(int(x), 2**62) for x in budgets], dtype=np.int64)
+        infos = (PlanInfo * nb)()
+        chain, cached, stage = self._alloc(nb)
+        check(fn(b.ctypes.data, nb, OBJECTIVE_CODE[objective], C.addressof(infos),
+                 chain.ctypes.data, cached.ctypes.data, stage.ctypes.data))
+        return [self._unpack(infos[i], chain[i], cached[i], stage[i]) for i in range(nb)]
+
+    def solve_level_sharded(self, comm: "Comm", budgets: list[int], objective: str):
+        """``solve`` with every level's targets split over the communicator's ranks."""
+        return self._solve_with(
+            lambda *a: lib().remat_solve_level_sharded(self.handle, comm.handle, *a),
+            budgets, objective)
 
     def min_feasible_budget(self, objective: str, probes_per_round: int = 8):
         info = PlanInfo()

@@ -220,6 +220,7 @@ struct remat_family_s {
   remat::DevBuf<long long> ML, TL, Mb, TLnb, base, foff;
   long long slots = 0;
   std::vector<long long> level_start;           // [n+2]
+  std::vector<long long> h_foff;                // host copy of foff (level sharding)
   std::vector<long long> level_maxR;            // [n+1]
   // DP state for up to nb_cap budgets
   int narrow = 0;                               // 32-bit row keys + 8 B entries
@@ -233,7 +234,14 @@ struct remat_family_s {
   remat::DevBuf<int> chain_idx;
   remat::DevBuf<u64> stage_bound;
   remat_timings timings{};
+  // the solve in flight (solve_begin .. solve_finish)
+  int cur_nb = 0, cur_objective = 0, cur_narrow = 0;
+  long long launches0 = 0, relax_launches = 0;
 
+  remat::DpView dp_view() const {
+    return remat::DpView{slots,    fe.p,     parent.p,  flen.p,  ccount.p, mmin.p,
+                         trans.p, npairs.p, budgets.p, IB, cur_objective == REMAT_MAXIMIZE};
+  }
   remat::FamilyView view() const {
     return remat::FamilyView{F, masks.p, bound.p, ML.p, TL.p, Mb.p, TLnb.p, base.p, foff.p};
   }
@@ -246,7 +254,12 @@ int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f);
 int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_t s,
                    long long* total_host);
 
-// relax.cu
+// relax.cu: a solve is begin, one call per level (targets [lo, hi) of the
+// level), finish; solve_batch runs all levels on one device
+int solve_begin(remat_family_s* f, const std::vector<long long>& budgets, int objective);
+int solve_level(remat_family_s* f, int lvl, long long lo, long long hi);
+int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64* cached_masks,
+                 long long* stage_memory);
 int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,
                 remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                 long long* stage_memory);

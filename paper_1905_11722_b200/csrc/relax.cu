@@ -115,7 +115,8 @@ struct Traits<false> {
 
 // Shared-memory carve-up of k_relax_tile (host and device agree on it).
 struct TileArgs {
-  long long jbase;  // first target of the level (= end of the predecessor range)
+  long long jbase;  // first target of this launch
+  long long pend;   // end of the predecessor range (= start of the level)
   int width;        // targets in the level
   int TJ;           // targets per tile
   int splits;       // CTAs per tile (they share the tile's predecessor chunks)
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kThreads)
   const int* flen_b = dp.flen + (size_t)b * F;
   const long long* mmin_b = dp.mmin + (size_t)b * F;
   const E* fe = reinterpret_cast<const E*>(dp.fe);
-  const long long pred_end = ta.jbase;
+  const long long pred_end = ta.pend;
   const long long nch = (pred_end + 31) / 32;
   unsigned* ctr = ta.ctr + (size_t)b * ta.tiles + tile;
   u64 my_trans = 0;  // lane jt accumulates target jt of the tile
@@ -721,11 +722,12 @@ __global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
 static constexpr int kSmemLimit = 200 * 1024;  // dynamic shared bytes per CTA
 static constexpr int kRowBudget = 64 * 1024;   // tile rows per CTA (4 CTAs/SM)
 
+// The solve in three phases so the level loop can be driven from outside
+// (level sharding, shard.cu): begin (buffers + the empty set), one call per
+// level for the targets [lo, hi) of that level, finish (reconstruction,
+// figures, statistics, copy-out).
 template <int W, bool NARROW>
-static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int objective,
-                   remat_plan_info* info, u64* chain_masks, u64* cached_masks,
-                   long long* stage_memory) {
-  using Key = typename Traits<NARROW>::Key;
+static int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int objective) {
   using E = typename Traits<NARROW>::E;
   remat_graph_s* g = f->g;
   cudaStream_t s = g->stream;
@@ -752,72 +754,103 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     attr_set = true;
   }
-  DpView dp{f->slots,  f->fe.p,   f->parent.p,  f->flen.p,    f->ccount.p, f->mmin.p,
-            f->trans.p, f->npairs.p, f->budgets.p, f->IB, objective == REMAT_MAXIMIZE};
-  FamilyView fv = f->view();
-  GraphView gv = g->view();
-  ClassView cv = g->classes();
-  const int K = cv.KT + cv.KM;
-  Events& ev = g->ev;
-  const long long launches0 = remat_kernel_launch_count();
+  f->cur_nb = nb;
+  f->cur_objective = objective;
+  f->cur_narrow = NARROW;
+  f->launches0 = remat_kernel_launch_count();
+  f->relax_launches = 0;
   RM_CUDA(cudaMemcpyAsync(f->budgets.p, budgets.data(), sizeof(long long) * nb,
                           cudaMemcpyHostToDevice, s));
-  RM_CUDA(cudaEventRecord(ev.e[3], s));
+  RM_CUDA(cudaEventRecord(g->ev.e[3], s));
+  // every per-member array starts zeroed so a level-sharded replica can be
+  // filled in any order; trans/npairs are accumulated atomically
   RM_CUDA(cudaMemsetAsync(f->trans.p, 0, sizeof(u64) * nb * F, s));
   RM_CUDA(cudaMemsetAsync(f->npairs.p, 0, sizeof(u64) * nb * F, s));
-  k_dp_init<NARROW><<<(nb + 127) / 128, 128, 0, s>>>(dp, F, nb);
+  RM_CUDA(cudaMemsetAsync(f->flen.p, 0, sizeof(int) * nb * F, s));
+  RM_CUDA(cudaMemsetAsync(f->ccount.p, 0, sizeof(int) * nb * F, s));
+  k_dp_init<NARROW><<<(nb + 127) / 128, 128, 0, s>>>(f->dp_view(), F, nb);
   RM_LAUNCHED();
-  long long relax_launches = 0;
+  return REMAT_OK;
+}
+
+template <int W, bool NARROW>
+static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
+  using Key = typename Traits<NARROW>::Key;
+  remat_graph_s* g = f->g;
+  cudaStream_t s = g->stream;
+  const int nb = f->cur_nb;
+  int rc;
+  const DpView dp = f->dp_view();
+  const FamilyView fv = f->view();
+  const GraphView gv = g->view();
+  const ClassView cv = g->classes();
+  const int K = cv.KT + cv.KM;
   static int num_sms = 0;
   if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
   const long long target_ctas = (long long)num_sms * 4;  // resident CTAs at 256 threads
-  for (int lvl = 1; lvl <= n; lvl++) {
-    const long long j0 = f->level_start[lvl], width = f->level_start[lvl + 1] - j0;
-    if (width == 0) continue;
-    const int R = (int)f->level_maxR[lvl];
-    // targets per tile: as many rows as fit the per-CTA row budget, <= width
-    int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ, width),
-                                      std::max<long long>(1, kRowBudget / ((long long)R * sizeof(Key))));
-    const long long nch = (j0 + 31) / 32;
-    // fewer targets per tile where the level is too small to give every
-    // resident warp a couple of (tile, chunk) tasks
-    const long long want = (long long)num_sms * 64;
-    while (TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
-    const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
-    TileArgs ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
-    if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
-    const long long tiles = (width + TJ - 1) / TJ;
-    // split the predecessor scan across CTAs when the level alone cannot fill
-    // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
-    long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
-    splits = std::max(1LL, std::min(splits, nch / kWarps));
-    ta.jbase = j0;
-    ta.width = (int)width;
-    ta.splits = (int)splits;
-    ta.grow = nullptr;
-    ta.rows_pb = (int)(tiles * TJ);
-    ta.tiles = (int)tiles;
-    if ((rc = f->ctr.ensure((size_t)nb * tiles)) < 0) return rc;
-    ta.ctr = f->ctr.p;
-    RM_CUDA(cudaMemsetAsync(ta.ctr, 0, sizeof(unsigned) * nb * tiles, s));
-    if (splits > 1 || !ta.smem_rows) {
-      const size_t cells = (size_t)nb * tiles * TJ * R;
-      if ((rc = f->rowscratch.ensure((cells * sizeof(Key) + 7) / 8)) < 0) return rc;
-      ta.grow = f->rowscratch.p;
-      k_fill<Key><<<(unsigned)std::min<size_t>((cells + 255) / 256, 4096), 256, 0, s>>>(
-          reinterpret_cast<Key*>(ta.grow), cells, Traits<NARROW>::INF);
-      RM_LAUNCHED();
-    }
-    k_relax_tile<W, NARROW><<<dim3((unsigned)(tiles * splits), (unsigned)nb), kThreads, ta.bytes,
-                              s>>>(fv, gv, cv, dp, ta);
+  const long long j0 = f->level_start[lvl];               // predecessors: [0, j0)
+  const long long width = hi - lo;
+  if (width <= 0) return REMAT_OK;
+  const int R = (int)f->level_maxR[lvl];
+  // targets per tile: as many rows as fit the per-CTA row budget, <= width
+  int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ, width),
+                                    std::max<long long>(1, kRowBudget / ((long long)R * sizeof(Key))));
+  const long long nch = (j0 + 31) / 32;
+  // fewer targets per tile where the level is too small to give every
+  // resident warp a couple of (tile, chunk) tasks
+  const long long want = (long long)num_sms * 64;
+  while (TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
+  const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
+  TileArgs ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
+  if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
+  const long long tiles = (width + TJ - 1) / TJ;
+  // split the predecessor scan across CTAs when the level alone cannot fill
+  // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
+  long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
+  splits = std::max(1LL, std::min(splits, nch / kWarps));
+  ta.jbase = lo;
+  ta.pend = j0;
+  ta.width = (int)width;
+  ta.splits = (int)splits;
+  ta.grow = nullptr;
+  ta.rows_pb = (int)(tiles * TJ);
+  ta.tiles = (int)tiles;
+  if ((rc = f->ctr.ensure((size_t)nb * tiles)) < 0) return rc;
+  ta.ctr = f->ctr.p;
+  RM_CUDA(cudaMemsetAsync(ta.ctr, 0, sizeof(unsigned) * nb * tiles, s));
+  if (splits > 1 || !ta.smem_rows) {
+    const size_t cells = (size_t)nb * tiles * TJ * R;
+    if ((rc = f->rowscratch.ensure((cells * sizeof(Key) + 7) / 8)) < 0) return rc;
+    ta.grow = f->rowscratch.p;
+    k_fill<Key><<<(unsigned)std::min<size_t>((cells + 255) / 256, 4096), 256, 0, s>>>(
+        reinterpret_cast<Key*>(ta.grow), cells, Traits<NARROW>::INF);
     RM_LAUNCHED();
-    relax_launches++;
-    if (ta.grow) {
-      k_finalize_rows<NARROW><<<dim3((unsigned)((width + kWarps - 1) / kWarps), (unsigned)nb),
-                                kThreads, 0, s>>>(fv, dp, j0, (int)width, ta.rows_pb, R, ta.grow);
-      RM_LAUNCHED();
-    }
   }
+  k_relax_tile<W, NARROW><<<dim3((unsigned)(tiles * splits), (unsigned)nb), kThreads, ta.bytes,
+                            s>>>(fv, gv, cv, dp, ta);
+  RM_LAUNCHED();
+  f->relax_launches++;
+  if (ta.grow) {
+    k_finalize_rows<NARROW><<<dim3((unsigned)((width + kWarps - 1) / kWarps), (unsigned)nb),
+                              kThreads, 0, s>>>(fv, dp, lo, (int)width, ta.rows_pb, R, ta.grow);
+    RM_LAUNCHED();
+  }
+  return REMAT_OK;
+}
+
+template <int W, bool NARROW>
+static int finish_w(remat_family_s* f, remat_plan_info* info, u64* chain_masks,
+                    u64* cached_masks, long long* stage_memory) {
+  remat_graph_s* g = f->g;
+  cudaStream_t s = g->stream;
+  const int nb = f->cur_nb;
+  const int n = g->n;
+  const long long F = f->F;
+  int rc;
+  const DpView dp = f->dp_view();
+  const FamilyView fv = f->view();
+  const GraphView gv = g->view();
+  Events& ev = g->ev;
   RM_CUDA(cudaEventRecord(ev.e[4], s));
   long long* expect = f->results.p;           // [nb][4]
   long long* stats = f->results.p + nb * 4;   // [nb][5]
@@ -858,8 +891,8 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   f->timings.relax_ms = relax_ms;
   f->timings.finish_ms = finish_ms;
   f->timings.total_ms = total_ms;
-  f->timings.relax_launches = relax_launches;
-  f->timings.kernel_launches = remat_kernel_launch_count() - launches0;
+  f->timings.relax_launches = f->relax_launches;
+  f->timings.kernel_launches = remat_kernel_launch_count() - f->launches0;
 
   const int Wu = g->W;
   for (int b = 0; b < nb; b++) {
@@ -892,19 +925,49 @@ static int solve_w(remat_family_s* f, const std::vector<long long>& budgets, int
   return REMAT_OK;
 }
 
-int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,
-                remat_plan_info* info, u64* chain_masks, u64* cached_masks,
-                long long* stage_memory) {
+template <typename Fn>
+static int dispatch_solve(remat_family_s* f, bool narrow, Fn&& fn) {
   int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
   dispatch_words(f->g->Wp, [&](auto wc) {
     constexpr int W = decltype(wc)::value;
-    // narrow pair records hold entry offsets within one budget's table as int32
-    if (f->narrow && f->slots < (1LL << 31))
-      rc = solve_w<W, true>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
-    else
-      rc = solve_w<W, false>(f, budgets, objective, info, chain_masks, cached_masks, stage_memory);
+    if (narrow) rc = fn(std::integral_constant<int, W>{}, std::true_type{});
+    else rc = fn(std::integral_constant<int, W>{}, std::false_type{});
   });
   return rc;
+}
+
+int solve_begin(remat_family_s* f, const std::vector<long long>& budgets, int objective) {
+  // narrow pair records hold entry offsets within one budget's table as int32
+  const bool narrow = f->narrow && f->slots < (1LL << 31);
+  return dispatch_solve(f, narrow, [&](auto wc, auto nc) {
+    return begin_w<decltype(wc)::value, decltype(nc)::value>(f, budgets, objective);
+  });
+}
+
+int solve_level(remat_family_s* f, int lvl, long long lo, long long hi) {
+  return dispatch_solve(f, f->cur_narrow, [&](auto wc, auto nc) {
+    return level_w<decltype(wc)::value, decltype(nc)::value>(f, lvl, lo, hi);
+  });
+}
+
+int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64* cached_masks,
+                 long long* stage_memory) {
+  return dispatch_solve(f, f->cur_narrow, [&](auto wc, auto nc) {
+    return finish_w<decltype(wc)::value, decltype(nc)::value>(f, info, chain_masks, cached_masks,
+                                                              stage_memory);
+  });
+}
+
+int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,
+                remat_plan_info* info, u64* chain_masks, u64* cached_masks,
+                long long* stage_memory) {
+  int rc = solve_begin(f, budgets, objective);
+  if (rc < 0) return rc;
+  for (int lvl = 1; lvl <= f->g->n; lvl++) {
+    rc = solve_level(f, lvl, f->level_start[lvl], f->level_start[lvl + 1]);
+    if (rc < 0) return rc;
+  }
+  return solve_finish(f, info, chain_masks, cached_masks, stage_memory);
 }
 
 }  // namespace remat

@@ -1,0 +1,393 @@
+// shard.cu — level-sharded exact DP across GPUs.
+//
+// The targets of every level are split into contiguous rank ranges; each rank
+// relaxes its share against its full replica of the finished levels, then the
+// ranks exchange the finished level with ONE all-gather: every rank packs the
+// frontier slots, back-pointers and per-member records (|frontier|, |cell|,
+// smallest m, Σ|frontier_i|, comparable pairs) of its targets into a staging
+// block of a level-wide common size, ncclAllGather over NVLink fills every
+// rank's receive buffer, and an unpack kernel writes the other ranks' blocks
+// into the local replica.  After the last level every replica holds the whole
+// table, so reconstruction, figures and statistics run unchanged on each rank
+// and every rank returns the same plan (bit-identical to one GPU: the targets'
+// values do not depend on who computed them).
+//
+// NCCL is loaded at run time (dlopen "libnccl.so.2"), so the library has no
+// link-time NCCL dependency and shares the copy torch.distributed already
+// loaded.  A loopback mode runs G replicas on ONE device with device copies in
+// place of the all-gather — the CI form of the same exchange.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "device.cuh"
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*errorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi* nccl_api(std::string* why) {
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      err = std::string("cannot load NCCL: ") + dlerror();
+      return;
+    }
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+    api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+    if (!api.getUniqueId || !api.commInitRank || !api.allGather || !api.commDestroy) {
+      err = "NCCL library lacks the required symbols";
+      return;
+    }
+    api.h = h;
+  });
+  if (!api.h) {
+    if (why) *why = err;
+    return nullptr;
+  }
+  return &api;
+}
+
+struct remat_comm_s {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0, device = 0;
+  remat::DevBuf<unsigned char> send, recv;
+};
+
+namespace remat {
+
+// contiguous share [lo, hi) of `width` targets starting at j0 for `rank`
+static inline void part(long long j0, long long width, int world, int rank, long long* lo,
+                        long long* hi) {
+  *lo = j0 + width * rank / world;
+  *hi = j0 + width * (rank + 1) / world;
+}
+
+// A batch of word copies (all offsets and lengths are multiples of 4 bytes).
+constexpr int kSegs = 48;
+struct Segs {
+  const unsigned* src[kSegs];
+  unsigned* dst[kSegs];
+  long long words[kSegs];
+  int n;
+};
+
+__global__ void k_copy_segs(Segs sg) {
+  for (int k = blockIdx.y; k < sg.n; k += gridDim.y) {
+    const unsigned* __restrict__ a = sg.src[k];
+    unsigned* __restrict__ b = sg.dst[k];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < sg.words[k];
+         i += (long long)gridDim.x * blockDim.x)
+      b[i] = a[i];
+  }
+}
+
+struct SegList {
+  std::vector<const void*> src;
+  std::vector<void*> dst;
+  std::vector<long long> bytes;
+  void add(const void* s, void* d, long long b) {
+    if (b <= 0) return;
+    src.push_back(s);
+    dst.push_back(d);
+    bytes.push_back(b);
+  }
+  int flush(cudaStream_t st) {
+    for (size_t k0 = 0; k0 < src.size(); k0 += kSegs) {
+      Segs sg{};
+      sg.n = (int)std::min<size_t>(kSegs, src.size() - k0);
+      long long mx = 0;
+      for (int k = 0; k < sg.n; k++) {
+        sg.src[k] = (const unsigned*)src[k0 + k];
+        sg.dst[k] = (unsigned*)dst[k0 + k];
+        sg.words[k] = bytes[k0 + k] / 4;
+        mx = std::max(mx, sg.words[k]);
+      }
+      const unsigned bx = (unsigned)std::min<long long>(std::max<long long>(1, (mx + 255) / 256), 512);
+      k_copy_segs<<<dim3(bx, (unsigned)sg.n), 256, 0, st>>>(sg);
+      RM_LAUNCHED();
+    }
+    src.clear();
+    dst.clear();
+    bytes.clear();
+    return REMAT_OK;
+  }
+};
+
+static inline long long al16(long long x) { return (x + 15) & ~15LL; }
+
+// Staging block of one rank for one budget: entries | parents | flen | ccount
+// | mmin | trans | npairs, each section sized for the level-wide maximum.
+struct Block {
+  long long emax, mmax, esize;
+  long long off_par, off_flen, off_cc, off_mmin, off_tr, off_np, bytes;
+  Block(long long emax_, long long mmax_, long long esize_)
+      : emax(emax_), mmax(mmax_), esize(esize_) {
+    off_par = al16(emax * esize);
+    off_flen = off_par + al16(emax * 4);
+    off_cc = off_flen + al16(mmax * 4);
+    off_mmin = off_cc + al16(mmax * 4);
+    off_tr = off_mmin + al16(mmax * 8);
+    off_np = off_tr + al16(mmax * 8);
+    bytes = off_np + al16(mmax * 8);
+  }
+};
+
+// Segments between a replica's arrays and a staging block (to_stage: pack).
+static void block_segments(remat_family_s* f, const Block& bk, int nb, long long a, long long b,
+                           unsigned char* stage, bool to_stage, SegList& sl) {
+  const long long F = f->F;
+  const long long e0 = f->h_foff[a], ne = f->h_foff[b] - f->h_foff[a], m = b - a;
+  for (int bb = 0; bb < nb; bb++) {
+    unsigned char* blk = stage + (size_t)bb * bk.bytes;
+    const size_t slot0 = (size_t)bb * f->slots + e0;
+    const size_t mem0 = (size_t)bb * F + a;
+    struct {
+      void* arr;
+      long long off, bytes;
+    } parts[] = {
+        {f->fe.p + slot0 * bk.esize, 0, ne * bk.esize},
+        {f->parent.p + slot0, bk.off_par, ne * 4},
+        {f->flen.p + mem0, bk.off_flen, m * 4},
+        {f->ccount.p + mem0, bk.off_cc, m * 4},
+        {f->mmin.p + mem0, bk.off_mmin, m * 8},
+        {f->trans.p + mem0, bk.off_tr, m * 8},
+        {f->npairs.p + mem0, bk.off_np, m * 8},
+    };
+    for (auto& p : parts) {
+      if (to_stage) sl.add(p.arr, blk + p.off, p.bytes);
+      else sl.add(blk + p.off, p.arr, p.bytes);
+    }
+  }
+}
+
+static int ensure_foff(remat_family_s* f) {
+  if ((long long)f->h_foff.size() == f->F + 1) return REMAT_OK;
+  f->h_foff.resize(f->F + 1);
+  RM_CUDA(cudaMemcpyAsync(f->h_foff.data(), f->foff.p, sizeof(long long) * (f->F + 1),
+                          cudaMemcpyDeviceToHost, f->g->stream));
+  RM_CUDA(cudaStreamSynchronize(f->g->stream));
+  return REMAT_OK;
+}
+
+static Block level_block(remat_family_s* f, int lvl, int world) {
+  const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
+  long long emax = 0, mmax = 0;
+  for (int r = 0; r < world; r++) {
+    long long lo, hi;
+    part(j0, w, world, r, &lo, &hi);
+    emax = std::max(emax, f->h_foff[hi] - f->h_foff[lo]);
+    mmax = std::max(mmax, hi - lo);
+  }
+  return Block(emax, mmax, f->cur_narrow ? (long long)sizeof(EntryN) : (long long)sizeof(EntryW));
+}
+
+static int check_same(remat_family_s* a, remat_family_s* b) {
+  if (a->F != b->F || a->g->n != b->g->n || a->slots != b->slots || a->narrow != b->narrow)
+    return fail(REMAT_ERR_VALUE, "level-sharded replicas must hold the same family");
+  return REMAT_OK;
+}
+
+}  // namespace remat
+
+using namespace remat;
+
+extern "C" {
+
+int remat_level_partition(int64_t level_start, int64_t width, int32_t world, int32_t rank,
+                          int64_t* begin, int64_t* end) {
+  if (world < 1 || rank < 0 || rank >= world || width < 0)
+    return fail(REMAT_ERR_VALUE, "bad partition arguments");
+  long long lo, hi;
+  part(level_start, width, world, rank, &lo, &hi);
+  *begin = lo;
+  *end = hi;
+  return REMAT_OK;
+}
+
+int remat_comm_unique_id(uint8_t* id) {
+  std::string why;
+  NcclApi* api = nccl_api(&why);
+  if (!api) return fail(REMAT_ERR_CUDA, why);
+  ncclUniqueId u;
+  ncclResult_t r = api->getUniqueId(&u);
+  if (r != ncclSuccess) return fail(REMAT_ERR_CUDA, std::string("ncclGetUniqueId: ") + api->errorString(r));
+  static_assert(sizeof(ncclUniqueId) == REMAT_COMM_ID_BYTES, "ncclUniqueId size");
+  std::memcpy(id, &u, sizeof u);
+  return REMAT_OK;
+}
+
+int remat_comm_create(const uint8_t* id, int32_t world, int32_t rank, int32_t device,
+                      remat_comm_t* out) {
+  if (world < 1 || rank < 0 || rank >= world) return fail(REMAT_ERR_VALUE, "bad world/rank");
+  std::string why;
+  NcclApi* api = nccl_api(&why);
+  if (!api) return fail(REMAT_ERR_CUDA, why);
+  RM_CUDA(cudaSetDevice(device));
+  auto* c = new remat_comm_s();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof u);
+  ncclResult_t r = api->commInitRank(&c->comm, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(REMAT_ERR_CUDA, std::string("ncclCommInitRank: ") + api->errorString(r));
+  }
+  *out = c;
+  return REMAT_OK;
+}
+
+int remat_comm_free(remat_comm_t c) {
+  if (!c) return REMAT_OK;
+  NcclApi* api = nccl_api(nullptr);
+  cudaSetDevice(c->device);
+  if (api && c->comm) api->commDestroy(c->comm);
+  delete c;
+  return REMAT_OK;
+}
+
+int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* budgets,
+                              int32_t nb, int32_t objective, remat_plan_info* info,
+                              uint64_t* chain_masks, uint64_t* cached_masks,
+                              int64_t* stage_memory) {
+  if (!c) return fail(REMAT_ERR_VALUE, "null communicator");
+  if (nb < 1) return fail(REMAT_ERR_VALUE, "need at least one budget");
+  if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
+    return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
+  remat_graph_s* g = f->g;
+  if (g->device != c->device) return fail(REMAT_ERR_VALUE, "family and communicator devices differ");
+  RM_CUDA(cudaSetDevice(g->device));
+  prepare_pool(g->device);
+  tls_stream = g->stream;
+  NcclApi* api = nccl_api(nullptr);
+  std::vector<long long> bs(nb);
+  for (int b = 0; b < nb; b++) {
+    if (budgets[b] < 0) return fail(REMAT_ERR_VALUE, "budget must be non-negative");
+    bs[b] = std::min<long long>(budgets[b], 2 * g->MV);
+  }
+  int rc;
+  if ((rc = ensure_foff(f)) < 0 || (rc = solve_begin(f, bs, objective)) < 0) return rc;
+  SegList sl;
+  for (int lvl = 1; lvl <= g->n; lvl++) {
+    const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
+    if (w == 0) continue;
+    long long lo, hi;
+    part(j0, w, c->world, c->rank, &lo, &hi);
+    if ((rc = solve_level(f, lvl, lo, hi)) < 0) return rc;
+    if (c->world == 1) continue;
+    const Block bk = level_block(f, lvl, c->world);
+    const size_t per = (size_t)nb * bk.bytes;
+    if ((rc = c->send.ensure(per)) < 0 || (rc = c->recv.ensure(per * c->world)) < 0) return rc;
+    block_segments(f, bk, nb, lo, hi, c->send.p, true, sl);
+    if ((rc = sl.flush(g->stream)) < 0) return rc;
+    ncclResult_t r = api->allGather(c->send.p, c->recv.p, per, ncclUint8, c->comm, g->stream);
+    if (r != ncclSuccess) return fail(REMAT_ERR_CUDA, std::string("ncclAllGather: ") + api->errorString(r));
+    for (int q = 0; q < c->world; q++) {
+      if (q == c->rank) continue;
+      long long qlo, qhi;
+      part(j0, w, c->world, q, &qlo, &qhi);
+      block_segments(f, bk, nb, qlo, qhi, c->recv.p + per * q, false, sl);
+    }
+    if ((rc = sl.flush(g->stream)) < 0) return rc;
+  }
+  if ((rc = solve_finish(f, info, (u64*)chain_masks, (u64*)cached_masks,
+                         (long long*)stage_memory)) < 0)
+    return rc;
+  for (int b = 0; b < nb; b++) info[b].budget = budgets[b];
+  return REMAT_OK;
+}
+
+int remat_solve_level_sharded_loopback(remat_family_t* fams, int32_t world,
+                                       const int64_t* budgets, int32_t nb, int32_t objective,
+                                       remat_plan_info* info, uint64_t* chain_masks,
+                                       uint64_t* cached_masks, int64_t* stage_memory) {
+  if (world < 1 || !fams) return fail(REMAT_ERR_VALUE, "need at least one replica");
+  if (nb < 1) return fail(REMAT_ERR_VALUE, "need at least one budget");
+  if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
+    return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
+  remat_family_s* f0 = fams[0];
+  remat_graph_s* g = f0->g;
+  int rc;
+  for (int r = 1; r < world; r++) {
+    if ((rc = check_same(f0, fams[r])) < 0) return rc;
+    if (fams[r]->g->device != g->device || fams[r]->g->stream != g->stream)
+      return fail(REMAT_ERR_VALUE, "loopback replicas must share one graph handle");
+  }
+  RM_CUDA(cudaSetDevice(g->device));
+  prepare_pool(g->device);
+  tls_stream = g->stream;
+  std::vector<long long> bs(nb);
+  for (int b = 0; b < nb; b++) {
+    if (budgets[b] < 0) return fail(REMAT_ERR_VALUE, "budget must be non-negative");
+    bs[b] = std::min<long long>(budgets[b], 2 * g->MV);
+  }
+  for (int r = 0; r < world; r++)
+    if ((rc = ensure_foff(fams[r])) < 0 || (rc = solve_begin(fams[r], bs, objective)) < 0)
+      return rc;
+  DevBuf<unsigned char> gathered;
+  SegList sl;
+  for (int lvl = 1; lvl <= g->n; lvl++) {
+    const long long j0 = f0->level_start[lvl], w = f0->level_start[lvl + 1] - j0;
+    if (w == 0) continue;
+    for (int r = 0; r < world; r++) {
+      long long lo, hi;
+      part(j0, w, world, r, &lo, &hi);
+      if ((rc = solve_level(fams[r], lvl, lo, hi)) < 0) return rc;
+    }
+    if (world == 1) continue;
+    const Block bk = level_block(f0, lvl, world);
+    const size_t per = (size_t)nb * bk.bytes;
+    if ((rc = gathered.ensure(per * world)) < 0) return rc;
+    // "all-gather": every replica packs its block straight into slot r
+    for (int r = 0; r < world; r++) {
+      long long lo, hi;
+      part(j0, w, world, r, &lo, &hi);
+      block_segments(fams[r], bk, nb, lo, hi, gathered.p + per * r, true, sl);
+    }
+    if ((rc = sl.flush(g->stream)) < 0) return rc;
+    for (int q = 0; q < world; q++)
+      for (int r = 0; r < world; r++) {
+        if (r == q) continue;
+        long long lo, hi;
+        part(j0, w, world, r, &lo, &hi);
+        block_segments(fams[q], bk, nb, lo, hi, gathered.p + per * r, false, sl);
+      }
+    if ((rc = sl.flush(g->stream)) < 0) return rc;
+  }
+  // every replica now holds the whole table; finish on each, report replica 0
+  std::vector<remat_plan_info> other(nb);
+  for (int r = world - 1; r >= 1; r--) {
+    if ((rc = solve_finish(fams[r], other.data(), nullptr, nullptr, nullptr)) < 0) return rc;
+  }
+  if ((rc = solve_finish(f0, info, (u64*)chain_masks, (u64*)cached_masks,
+                         (long long*)stage_memory)) < 0)
+    return rc;
+  for (int b = 0; b < nb; b++) {
+    info[b].budget = budgets[b];
+    if (world > 1 && (other[b].objective_value != info[b].objective_value ||
+                      other[b].stats.transitions != info[b].stats.transitions ||
+                      other[b].status != info[b].status))
+      return fail(REMAT_ERR_INTERNAL, "level-sharded replicas disagree");
+  }
+  return REMAT_OK;
+}
+
+}  // extern "C"
