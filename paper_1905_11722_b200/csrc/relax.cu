@@ -505,16 +505,41 @@ __global__ void __launch_bounds__(kThreads)
     // smem: rows addressed as 32-bit shared-window offsets; global: pointers
     auto relax_items = [&](Key* __restrict__ rw, const unsigned rs, const bool smem) {
       int kbase = -1;
-      for (int r = 0; r < tot; r += 32) {
+      auto map_step = [&](int r) {  // warp-uniform call
         const unsigned d = (unsigned)(start - r);
         const unsigned smask = __reduce_or_sync(kFull, d < 32u ? 1u << d : 0u);
         const int k = kbase + __popc(smask & le);
         kbase += __popc(smask);
-        if (r + lane < tot) {
-          const PredRec rec = wrec[k];
-          unsigned t;
-          MT m;
-          Traits<NARROW>::load(fe + (rec.base + r + lane), t, m);
+        return k;
+      };
+      // software-pipelined: the entry of step r+32 is in flight (L2) while
+      // the targets of step r are relaxed
+      PredRec rec{};
+      unsigned t = 0;
+      MT m = 0;
+      bool v = false;
+      {
+        const int k = map_step(0);
+        v = lane < tot;
+        if (v) {
+          rec = wrec[k];
+          Traits<NARROW>::load(fe + (rec.base + lane), t, m);
+        }
+      }
+      for (int r = 0; r < tot; r += 32) {
+        PredRec recn{};
+        unsigned tn = 0;
+        MT mn = 0;
+        bool vn = false;
+        if (r + 32 < tot) {
+          const int kn = map_step(r + 32);
+          vn = r + 32 + lane < tot;
+          if (vn) {
+            recn = wrec[kn];
+            Traits<NARROW>::load(fe + (recn.base + r + 32 + lane), tn, mn);
+          }
+        }
+        if (v) {
           const Key mk = (Key)m << IB;
           const Q* qe = wq + rec.q1;
           for (const Q* qp = wq + rec.q0; qp < qe; ++qp) {
@@ -528,6 +553,10 @@ __global__ void __launch_bounds__(kThreads)
             if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
           }
         }
+        rec = recn;
+        t = tn;
+        m = mn;
+        v = vn;
       }
     };
     if (srow)
