@@ -426,17 +426,25 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 
 // K1 as ONE cooperative launch with one grid barrier per level (SURVEY §7
 // hard part 5: n = 516 dependent levels at C5).  Level k's members sit
-// UNSORTED in a ping-pong buffer U_k (with their maximal-element sets); in
-// the step for level k every warp emits canonical children of (member, 32-node
-// chunk) tasks into U_{k+1} at atomically reserved positions, while the same
-// step rank-sorts U_k into the family at ls[k] — both only read U_k, and the
-// emission order is irrelevant because U_{k+1} is ranked in the next step.
+// UNSORTED (mask + maximal-element set) in buffer U[k % 3].  Grid step k runs
+// three independent jobs, load-balanced over every block:
+//   (a) canonical children of level k, one (member, 32-node chunk) task per
+//       warp, appended to U[(k+1) % 3] at atomically reserved positions (the
+//       emission order is irrelevant: the level is ranked afterwards);
+//   (b) partial ranks of level k: (element tile, comparison tile) tasks of
+//       256 x 256 mask comparisons, atomically summed into rank[k % 3]
+//       (rank(i) = #{q : mask_q < mask_i}, all masks of a level distinct);
+//   (c) scatter of level k-1 into the family at ls[k-1] + rank, using the
+//       ranks completed in step k-1.
+// Buffers rotate over three slots, so each is written one step after its
+// last reader finished.
 //   ctr[k]    |level k| (ctr[0] = 1: the empty set, pre-set by the host)
 //   status[0] 1 when the lattice exceeds `cap` (LatticeTooLargeError)
 template <int W>
 __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds, int n,
                                                   long long cap, u64* __restrict__ fam,
-                                                  u64* __restrict__ U0, u64* __restrict__ U1,
+                                                  u64* __restrict__ U, long long ucap,
+                                                  unsigned* __restrict__ rank,
                                                   long long* __restrict__ ctr,
                                                   long long* __restrict__ ls,
                                                   int* __restrict__ status) {
@@ -446,18 +454,30 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
   const int lane = threadIdx.x & 31;
   const long long nwarps = (long long)gridDim.x * 8;
   const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const long long gt = (long long)blockIdx.x * 256 + threadIdx.x;
+  const long long nthreads = (long long)gridDim.x * 256;
   const int nch = (n + 31) / 32;
-  long long base = 0;  // ls[k]
-  for (int k = 0; k <= n; k++) {
-    const long long N = *((volatile long long*)(ctr + k));
+  long long base = 0, prev_base = 0, prevN = 0;  // ls[k], ls[k-1], |level k-1|
+  for (int k = 0; k <= n + 1; k++) {
+    const long long N = k <= n ? *((volatile long long*)(ctr + k)) : 0;
     if (base + N > cap) {  // uniform: every block read the same counters
       if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = 1;
       return;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) ls[k] = base;
-    const u64* cur = (k & 1) ? U1 : U0;  // [N][2W]: mask, maximal elements
-    u64* nxt = (k & 1) ? U0 : U1;
-    const long long room = cap - base - N;  // children that still fit under the cap
+    if (blockIdx.x == 0 && threadIdx.x == 0 && k <= n) ls[k] = base;
+    const u64* cur = U + (size_t)(k % 3) * ucap * 2 * W;   // [N][2W]
+    u64* nxt = U + (size_t)((k + 1) % 3) * ucap * 2 * W;
+    const u64* prv = U + (size_t)((k + 2) % 3) * ucap * 2 * W;
+    unsigned* rk = rank + (size_t)(k % 3) * ucap;
+    unsigned* rkp = rank + (size_t)((k + 2) % 3) * ucap;
+    const long long room = min(cap - base - N, ucap);  // children that fit
+    // (c) scatter level k-1, leaving its rank slot zeroed for level k+2
+    for (long long i = gt; i < prevN; i += nthreads) {
+      const long long at = prev_base + rkp[i];
+      rkp[i] = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) fam[at * W + w] = prv[i * 2 * W + w];
+    }
     // (a) canonical children of level k
     if (k < n)
       for (long long task = gw; task < N * nch; task += nwarps) {
@@ -473,7 +493,9 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
         const unsigned bal = __ballot_sync(kFull, ok);
         if (!bal) continue;
         unsigned long long at0 = 0;
-        if (lane == 0) at0 = atomicAdd(reinterpret_cast<unsigned long long*>(ctr + k + 1), (unsigned long long)__popc(bal));
+        if (lane == 0)
+          at0 = atomicAdd(reinterpret_cast<unsigned long long*>(ctr + k + 1),
+                          (unsigned long long)__popc(bal));
         at0 = __shfl_sync(kFull, at0, 0);
         const long long at = (long long)at0 + __popc(bal & ((1u << lane) - 1));
         if (ok && at < room) {
@@ -484,14 +506,12 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
           }
         }
       }
-    // (b) rank-sort level k by mask value: rank(i) = #{q : mask_q < mask_i}
-    for (long long i0 = (long long)blockIdx.x * 256; i0 < N; i0 += (long long)gridDim.x * 256) {
-      const long long i = i0 + threadIdx.x;
-      u64 me[W];
-#pragma unroll
-      for (int w = 0; w < W; w++) me[w] = i < N ? cur[i * 2 * W + w] : 0ull;
-      long long rank = 0;
-      for (long long t0 = 0; t0 < N; t0 += 256) {
+    // (b) partial ranks of level k over (element tile, comparison tile) tasks
+    if (k <= n) {
+      const long long nt = (N + 255) / 256;
+      for (long long task = blockIdx.x; task < nt * nt; task += gridDim.x) {
+        const long long it = task / nt, tt = task - it * nt;
+        const long long i = it * 256 + threadIdx.x, t0 = tt * 256;
         const long long c = min(256LL, N - t0);
         __syncthreads();
         for (int e = threadIdx.x; e < c * W; e += 256) {
@@ -499,13 +519,18 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
           tile[e] = cur[(t0 + q) * 2 * W + (e - q * W)];
         }
         __syncthreads();
-        if (i < N)
-          for (int q = 0; q < c; q++) rank += mask_less<W>(tile + q * W, me);
-      }
-      if (i < N)
+        if (i < N) {
+          u64 me[W];
 #pragma unroll
-        for (int w = 0; w < W; w++) fam[(base + rank) * W + w] = me[w];
+          for (int w = 0; w < W; w++) me[w] = cur[i * 2 * W + w];
+          unsigned r = 0;
+          for (int q = 0; q < c; q++) r += mask_less<W>(tile + q * W, me);
+          if (r) atomicAdd(rk + i, r);
+        }
+      }
     }
+    prev_base = base;
+    prevN = k <= n ? N : 0;
     base += N;
     grid.sync();
   }
@@ -517,36 +542,44 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
                           std::vector<long long>& level_start) {
   cudaStream_t s = g->stream;
   const int n = g->n;
-  // sized for the cap (a larger lattice raises LatticeTooLargeError):
-  // family cap x 8W bytes plus two level buffers of cap x 16W bytes in HBM
+  // the family is sized for the cap (a larger lattice raises
+  // LatticeTooLargeError); the three level buffers hold one level each, and
+  // no level is wider than C(n, n/2) nor than the cap
   const long long Fcap = std::max<long long>(cap, n + 1);
+  long double binom = 1;
+  for (int i = 1; i <= n / 2; i++) binom = binom * (n - n / 2 + i) / i;
+  const long long ucap = (long long)std::min<long double>((long double)Fcap, binom + 1);
   int rc;
-  DevBuf<u64> U0, U1;
+  DevBuf<u64> U;
+  DevBuf<unsigned> rank;
   DevBuf<int> status;
   DevBuf<long long> ctr, ls;
-  static int blocks_per_sm[17] = {}, num_sms = 0;
+  static int num_sms = 0;
   if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
-  if (!blocks_per_sm[W]) {
-    RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm[W], k_enum_all<W>, 256, 0));
-    blocks_per_sm[W] = std::max(1, std::min(blocks_per_sm[W], 4));
-  }
-  const int nblk = num_sms * blocks_per_sm[W];
-  if ((rc = fam.ensure((size_t)Fcap * W)) < 0 || (rc = U0.ensure((size_t)Fcap * 2 * W)) < 0 ||
-      (rc = U1.ensure((size_t)Fcap * 2 * W)) < 0 || (rc = ctr.ensure(n + 2)) < 0 ||
+  int bps = 0;
+  RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_enum_all<W>, 256, 0));
+  if (bps < 1) return fail(REMAT_ERR_CUDA, "enumeration kernel cannot be resident");
+  // one block per SM keeps the per-level grid barrier cheap
+  const int nblk = num_sms;
+  if ((rc = fam.ensure((size_t)Fcap * W)) < 0 || (rc = U.ensure((size_t)3 * ucap * 2 * W)) < 0 ||
+      (rc = rank.ensure((size_t)3 * ucap)) < 0 || (rc = ctr.ensure(n + 2)) < 0 ||
       (rc = ls.ensure(n + 2)) < 0 || (rc = status.ensure(1)) < 0)
     return rc;
-  RM_CUDA(cudaMemsetAsync(U0.p, 0, sizeof(u64) * 2 * W, s));  // the empty set, no maximal elements
+  RM_CUDA(cudaMemsetAsync(U.p, 0, sizeof(u64) * 2 * W, s));  // the empty set, no maximal elements
+  RM_CUDA(cudaMemsetAsync(rank.p, 0, sizeof(unsigned) * 3 * ucap, s));
   RM_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(long long) * (n + 2), s));
   RM_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
   const long long one = 1;
   RM_CUDA(cudaMemcpyAsync(ctr.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
   const u64* preds = g->preds.p;
-  u64 *a0 = fam.p, *a1 = U0.p, *a2 = U1.p;
+  u64 *a0 = fam.p, *a1 = U.p;
+  long long uc = ucap;
+  unsigned* a2 = rank.p;
   long long *a3 = ctr.p, *a4 = ls.p;
   int* a5 = status.p;
   int nn = n;
   long long cp = cap;
-  void* args[] = {(void*)&preds, &nn, &cp, &a0, &a1, &a2, &a3, &a4, &a5};
+  void* args[] = {(void*)&preds, &nn, &cp, &a0, &a1, &uc, &a2, &a3, &a4, &a5};
   RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_enum_all<W>, dim3(nblk), dim3(256), args, 0,
                                       s));
   RM_LAUNCHED();

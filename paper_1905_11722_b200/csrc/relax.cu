@@ -190,8 +190,7 @@ __device__ __forceinline__ void relax_smem(unsigned a, unsigned key, bool ok) {
       "setp.ne.u32 o, %2, 0;\n\t"
       "setp.lt.and.u32 q, %1, c, o;\n\t"
       "@q red.shared.min.u32 [%0], %1;\n\t}"
-      ::"r"(a), "r"(key), "r"((unsigned)ok)
-      : "memory");
+      ::"r"(a), "r"(key), "r"((unsigned)ok));
 }
 
 template <typename T>
