@@ -193,6 +193,23 @@ __device__ __forceinline__ void relax_smem(unsigned a, unsigned key, bool ok) {
       ::"r"(a), "r"(key), "r"((unsigned)ok));
 }
 
+// Two candidates at once (two rows of the tile, so never the same slot): both
+// probes are issued before either update.
+__device__ __forceinline__ void relax_smem2(unsigned a0, unsigned k0, bool ok0, unsigned a1,
+                                            unsigned k1, bool ok1) {
+  asm volatile(
+      "{\n\t.reg .pred o0, o1, q0, q1;\n\t.reg .u32 c0, c1;\n\t"
+      "ld.shared.u32 c0, [%0];\n\t"
+      "ld.shared.u32 c1, [%3];\n\t"
+      "setp.ne.u32 o0, %2, 0;\n\t"
+      "setp.ne.u32 o1, %5, 0;\n\t"
+      "setp.lt.and.u32 q0, %1, c0, o0;\n\t"
+      "setp.lt.and.u32 q1, %4, c1, o1;\n\t"
+      "@q0 red.shared.min.u32 [%0], %1;\n\t"
+      "@q1 red.shared.min.u32 [%3], %4;\n\t}"
+      ::"r"(a0), "r"(k0), "r"((unsigned)ok0), "r"(a1), "r"(k1), "r"((unsigned)ok1));
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_min_all(T v) {
 #pragma unroll
@@ -541,14 +558,23 @@ __global__ void __launch_bounds__(kThreads)
         if (v) {
           const Key mk = (Key)m << IB;
           const Q* qe = wq + rec.q1;
-          for (const Q* qp = wq + rec.q0; qp < qe; ++qp) {
-            const Q p = Traits<NARROW>::lds(qp);
-            if constexpr (NARROW) {
-              if (smem) {
-                relax_smem(rs + 4u * (t + (unsigned)p.dtr), mk + p.kb, m <= p.cap);
-                continue;
+          const Q* qp = wq + rec.q0;
+          if constexpr (NARROW) {
+            if (smem) {
+              for (; qp + 1 < qe; qp += 2) {
+                const Q p0 = Traits<NARROW>::lds(qp), p1 = Traits<NARROW>::lds(qp + 1);
+                relax_smem2(rs + 4u * (t + (unsigned)p0.dtr), mk + p0.kb, m <= p0.cap,
+                            rs + 4u * (t + (unsigned)p1.dtr), mk + p1.kb, m <= p1.cap);
               }
+              if (qp < qe) {
+                const Q p = Traits<NARROW>::lds(qp);
+                relax_smem(rs + 4u * (t + (unsigned)p.dtr), mk + p.kb, m <= p.cap);
+              }
+              qp = qe;
             }
+          }
+          for (; qp < qe; ++qp) {
+            const Q p = Traits<NARROW>::lds(qp);
             if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
           }
         }
