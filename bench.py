@@ -224,16 +224,30 @@ def run_ours(args, world, rank, local):
     from paper_1905_11722_b200._native import DeviceFamily, DeviceGraph, kernel_launches
 
     g, name = workload(args)
-    # budget sharding: rank r solves budget 2·M(V) − r of the sweep (all
-    # budgets >= the single-segment need; per-rank work is near-identical)
-    budget = 2 * g.total_memory - rank
+    levels = world > 1 and args.parallel == "levels"
+    if levels:
+        # level sharding: every rank works on the SAME solve (budget 2·M(V));
+        # each level's targets are split over the ranks, one NCCL all-gather
+        # per level (paper_1905_11722_b200/shard.py)
+        from paper_1905_11722_b200._native import Comm
+        from paper_1905_11722_b200.shard import exchange_unique_id
+
+        budget = 2 * g.total_memory
+        comm = Comm(exchange_unique_id(), world, rank, local)
+    else:
+        # budget sharding: rank r solves budget 2·M(V) − r of the sweep (all
+        # budgets >= the single-segment need; per-rank work is near-identical)
+        budget = 2 * g.total_memory - rank
     dg = DeviceGraph(g, local)
     stream = torch.cuda.ExternalStream(dg.stream(), device=local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
     def step():
         fam = DeviceFamily(dg, "full", 2_000_000)
-        info = fam.solve([budget], "minimize")[0][0]
+        if levels:
+            info = fam.solve_level_sharded(comm, [budget], "minimize")[0][0]
+        else:
+            info = fam.solve([budget], "minimize")[0][0]
         return fam, info
 
     for _ in range(args.warmup):
@@ -268,7 +282,8 @@ def run_ours(args, world, rank, local):
             fam.close()
     launches = kernel_launches() - launches0
     ms_max = allmax(world, dev_ms)
-    X_all = allsum(world, X * args.steps)
+    # level sharding: all ranks share one solve, so its transitions count once
+    X_all = X * args.steps if levels else allsum(world, X * args.steps)
     value = X_all / (ms_max / 1e3)
 
     # end-to-end through the public API (graph in host memory, plan back on host)
@@ -284,6 +299,19 @@ def run_ours(args, world, rank, local):
         e2e_t.append(time.perf_counter() - t0)
     e2e_s = allmax(world, sum(e2e_t) / len(e2e_t))
     e2e_value = allsum(world, plan.stats.transitions) / e2e_s
+    if levels:  # the public API of the level-sharded path
+        from paper_1905_11722_b200.shard import LevelShardedSolver
+
+        e2e_t = []
+        for k in range(max(1, min(args.steps, 5))):
+            barrier(world)
+            t0 = time.perf_counter()
+            ls = LevelShardedSolver(g, "full")
+            plan = ls.plan(budget)
+            ls.close()
+            e2e_t.append(time.perf_counter() - t0)
+        e2e_s = allmax(world, sum(e2e_t) / len(e2e_t))
+        e2e_value = plan.stats.transitions / e2e_s
     d2h = (g.n + 1) * 8 * ((g.n + 63) // 64) * 2 + (g.n + 1) * 8 + 64
 
     cpu = None
@@ -303,24 +331,25 @@ def run_ours(args, world, rank, local):
     achieved = q_relax / relax_s / 1e9
     prof = ROOT / "profiles" / "relax_traffic.json"
     traffic = None
-    if prof.exists():
-        d = json.loads(prof.read_text())
-        if d.get("workload") == name:
-            traffic = d.get("dram_bytes_per_launch")
+    if prof.exists():  # ncu capture of the same workload (tools/gpu_traffic.sh)
+        rec = json.loads(prof.read_text()).get(name)
+        if rec:
+            traffic = rec["dram_bytes_per_launch"]
     line = {
         "metric": "exact-DP transitions/s (end-to-end solve)",
         "value": value, "unit": "transitions/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if levels else "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic",
         "config": {"workload": name, "n": g.n, "family_size": F, "budget": budget,
                    "transitions_per_step": X, "comparable_pairs": P, "table_entries": E,
-                   "parallelism": f"budget-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"level-sharded x{world} (NCCL all-gather per level)" if levels
+                                   else f"budget-sharded x{world}" if world > 1 else "single GPU"),
                    "l2": "flushed (256 MiB write) between steps",
                    "phase_ms": {"enumerate": enum_ms / args.steps,
                                 "precompute": pre_ms / args.steps,
                                 "relax": relax_ms / args.steps}},
-        "roofline": {"bound": "hbm", "kernel": "k_relax_level",
+        "roofline": {"bound": "hbm", "kernel": "k_relax_tile",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "peak_source": pk["source"],
@@ -333,6 +362,8 @@ def run_ours(args, world, rank, local):
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
+    if levels:
+        comm.close()
 
 
 def main():
@@ -345,6 +376,9 @@ def main():
     ap.add_argument("--skip-len", type=int, default=8)
     ap.add_argument("--edge-prob", type=float, default=0.3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--parallel", choices=("budgets", "levels"), default="budgets",
+                    help="N>1: independent budgets per GPU (weak) or one solve with every "
+                         "level's targets sharded over the GPUs (strong)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
