@@ -354,7 +354,11 @@ def run_ours(args, world, rank, local):
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
                      "peak_source": pk["source"],
                      "bytes_per_launch": q_relax / max(1, relax_launches // args.steps),
-                     "avg_launch_ms": relax_ms / max(1, relax_launches)},
+                     "avg_launch_ms": relax_ms / max(1, relax_launches),
+                     "note": ("achieved = SURVEY 8(d) algorithmic bytes 12X+(16W+16)P+16E of the "
+                              "relaxation / its device time; the table is L2-resident (traffic = "
+                              "measured DRAM bytes per launch), so the binding resource is SM "
+                              "issue on shared-memory row probes, see profiles/")},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s},
