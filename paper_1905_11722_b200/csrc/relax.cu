@@ -49,6 +49,7 @@ namespace remat {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxTJ = 8;    // targets per tile (one comparable bit each, <= 32)
+constexpr int kDenseLanes = 16;  // lanes with a pair for lane = predecessor constants
 
 // One relaxable (predecessor, target) pair of a warp's current group.
 struct __align__(16) PairQN {  // narrow: one LDS.128
@@ -393,105 +394,126 @@ __global__ void __launch_bounds__(kThreads)
 
   // Every CTA of the tile pulls 32-predecessor chunks from the tile's counter,
   // so slices finish together and CTAs of a late wave find nothing left.
+  // Pair constants of (predecessor i, tile target jt) -> record q; true iff
+  // some frontier entry of i can pass the budget test (cap >= its smallest m).
+  auto pair_q = [&](const u64 (&Li)[W], long long ii, int jt, long long MLi, long long TLi,
+                    long long mmi, Q& q) {
+    long long ts = 0, ms = 0;
+    if (tcls[jt]) {
+      const u64* bj = bjc + (size_t)jt * K * W;
+      for (int cc = 0; cc < K; cc++) {
+        int pc = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[cc * W + w]);
+        if (cc < KT) ts += __ldg(cv.coefT + cc) * pc;
+        else ms += __ldg(cv.coefM + cc - KT) * pc;
+      }
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        u64 x = Li[w] & tB[jt * W + w];
+        while (x) {
+          const int v = w * 64 + __ffsll((long long)x) - 1;
+          x &= x - 1;
+          ts += __ldg(g.T + v);
+          ms += __ldg(g.M + v);
+        }
+      }
+    }
+    const long long fixed = 2 * (tc[jt * 4 + 0] - MLi) + tc[jt * 4 + 1];
+    const long long dt = tc[jt * 4 + 2] - TLi + ts;
+    const long long dm = tc[jt * 4 + 3] - ms;
+    const long long cap = B - fixed;
+    q.cap = (MT)max(cap, 0LL);
+    q.base = 0;
+    q.kb = (Key)(((u64)dm << IB) | (u64)ii);
+    q.dtr = jt * R + (int)dt;
+    return cap >= mmi;
+  };
+
   while (true) {
     unsigned got = 0;
     if (lane == 0) got = atomicAdd(ctr, 1u);
     const long long ch = __shfl_sync(kFull, got, 0);
     if (ch >= nch) break;
     worked = true;
+    // lane = predecessor i: its set and scalars in one round of loads
     const long long i = ch * 32 + lane;
-    unsigned mask = 0;
+    u64 Li[W];
     int fl = 0;
+    long long MLi = 0, TLi = 0, mmi = 0, foffi = 0;
+    unsigned mask = 0;
     if (i < pred_end) {
-      u64 Li[W];
 #pragma unroll
       for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + i);
+      fl = flen_b[i];
+      mmi = mmin_b[i];
+      MLi = __ldg(fv.ML + i);
+      TLi = __ldg(fv.TL + i);
+      foffi = __ldg(fv.foff + i);
       for (int jt = 0; jt < ntj; jt++) {
         u64 acc = 0;
 #pragma unroll
         for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
         mask |= (acc == 0 ? 1u : 0u) << jt;
       }
-      if (mask) fl = flen_b[i];
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; w++) Li[w] = 0;
     }
     if (!__any_sync(kFull, mask)) continue;
+    // per target: statistics, then the pair constants — computed right here
+    // (lane = predecessor, no reload) when most lanes hold a pair, else
+    // deferred to a compacted list (lane = pair) so sparse targets do not
+    // serialise the warp
+    Q* myq = wq + lane * TJ;
+    int npq = 0;
+    unsigned sparse = 0;
     for (int jt = 0; jt < ntj; jt++) {
       const bool bit = (mask >> jt) & 1u;
-      const unsigned np = __popc(__ballot_sync(kFull, bit));
+      const unsigned cm = __ballot_sync(kFull, bit);
       const unsigned tr = __reduce_add_sync(kFull, bit ? (unsigned)fl : 0u);
       if (lane == jt) {
-        my_pairs += np;
+        my_pairs += __popc(cm);
         my_trans += tr;
       }
+      const bool want = bit && fl > 0;
+      const unsigned wm = __ballot_sync(kFull, want);
+      if (__popc(wm) >= kDenseLanes) {
+        if (want) {
+          Q q;
+          if (pair_q(Li, i, jt, MLi, TLi, mmi, q)) myq[npq++] = q;
+        }
+      } else if (want) {
+        sparse |= 1u << jt;
+      }
     }
-    // pairs (predecessor lane, target) in predecessor-major order
-    unsigned pm = fl > 0 ? mask : 0u;
-    const int cnt = __popc(pm);
-    const int cincl = warp_inclusive_sum(cnt);
-    const int npair = __shfl_sync(kFull, cincl, 31);
-    if (npair == 0) continue;
+    wpc[lane] = npq;
+    const int scnt = __popc(sparse);
+    const int sincl = warp_inclusive_sum(scnt);
+    const int nsp = __shfl_sync(kFull, sincl, 31);
     {
-      int pos = cincl - cnt;
-      while (pm) {
-        const int jt = __ffs(pm) - 1;
-        pm &= pm - 1;
+      int pos = sincl - scnt;
+      unsigned x = sparse;
+      while (x) {
+        const int jt = __ffs(x) - 1;
+        x &= x - 1;
         wpairs[pos++] = (unsigned short)((lane << 5) | jt);
       }
     }
-    wpc[lane] = 0;
     __syncwarp();
-    // pair constants (lane = pair); budget-feasible pairs are kept, in order
-    int qn = 0;
-    for (int g0 = 0; g0 < npair; g0 += 32) {
-      bool ok = false;
-      Q q{};
-      int pl = 0;
-      if (lane < npair - g0) {
+    for (int g0 = 0; g0 < nsp; g0 += 32) {
+      if (lane < nsp - g0) {
         const int pr = wpairs[g0 + lane];
-        const int jt = pr & 31;
-        pl = pr >> 5;
+        const int jt = pr & 31, pl = pr >> 5;
         const long long ii = ch * 32 + pl;
-        u64 Li[W];
+        u64 Lp[W];
 #pragma unroll
-        for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + ii);
-        long long ts = 0, ms = 0;
-        if (tcls[jt]) {
-          const u64* bj = bjc + (size_t)jt * K * W;
-          for (int cc = 0; cc < K; cc++) {
-            int pc = 0;
-#pragma unroll
-            for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[cc * W + w]);
-            if (cc < KT) ts += __ldg(cv.coefT + cc) * pc;
-            else ms += __ldg(cv.coefM + cc - KT) * pc;
-          }
-        } else {
-#pragma unroll
-          for (int w = 0; w < W; w++) {
-            u64 x = Li[w] & tB[jt * W + w];
-            while (x) {
-              const int v = w * 64 + __ffsll((long long)x) - 1;
-              x &= x - 1;
-              ts += __ldg(g.T + v);
-              ms += __ldg(g.M + v);
-            }
-          }
-        }
-        const long long fixed = 2 * (tc[jt * 4 + 0] - __ldg(fv.ML + ii)) + tc[jt * 4 + 1];
-        const long long dt = tc[jt * 4 + 2] - __ldg(fv.TL + ii) + ts;
-        const long long dm = tc[jt * 4 + 3] - ms;
-        const long long cap = B - fixed;
-        ok = cap >= mmin_b[ii];
-        q.cap = (MT)max(cap, 0LL);
-        q.base = 0;
-        q.kb = (Key)(((u64)dm << IB) | (u64)ii);
-        q.dtr = jt * R + (int)dt;
+        for (int w = 0; w < W; w++) Lp[w] = __ldg(fv.masks + (size_t)w * F + ii);
+        Q q;
+        if (pair_q(Lp, ii, jt, __ldg(fv.ML + ii), __ldg(fv.TL + ii), mmin_b[ii], q))
+          wq[pl * TJ + atomicAdd(wpc + pl, 1)] = q;
       }
-      const unsigned okm = __ballot_sync(kFull, ok);
-      if (ok) {
-        wq[qn + __popc(okm & lt)] = q;
-        atomicAdd(wpc + pl, 1);
-      }
-      qn += __popc(okm);
     }
     __syncwarp();
     // items = (predecessor, frontier entry), lane = predecessor again
@@ -499,15 +521,14 @@ __global__ void __launch_bounds__(kThreads)
     const int c = pc > 0 ? fl : 0;
     const unsigned has = __ballot_sync(kFull, c > 0);
     if (!has) continue;
-    const int pincl = warp_inclusive_sum(pc);
     const int iincl = warp_inclusive_sum(c);
     const int tot = __shfl_sync(kFull, iincl, 31);
     const int start = c > 0 ? iincl - c : INT_MAX;
     if (c > 0) {
       PredRec rc;
-      rc.base = fbase + __ldg(fv.foff + i) - (iincl - c);
-      rc.q0 = pincl - pc;
-      rc.q1 = pincl;
+      rc.base = fbase + foffi - (iincl - c);
+      rc.q0 = lane * TJ;
+      rc.q1 = lane * TJ + pc;
       wrec[__popc(has & lt)] = rc;
     }
     __syncwarp();
