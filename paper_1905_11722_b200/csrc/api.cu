@@ -93,6 +93,59 @@ static bool weight_classes(const std::vector<long long>& cost, int n, int Wp,
   return true;
 }
 
+// Classes for both weights at once: (mask, cT, cM) with
+// T_v = Σ_{c ∋ v} cT_c and M_v = Σ_{c ∋ v} cM_c.  Either the joint partition
+// by (T_v, M_v) value pairs, or the T and M decompositions side by side with
+// identical masks merged — whichever has fewer classes (uniform costs: one
+// class, so a weighted popcount pair is a single popcount).
+static bool joint_classes(const std::vector<long long>& T, const std::vector<long long>& M, int n,
+                          int Wp, std::vector<u64>& cls, std::vector<long long>& coef) {
+  std::map<std::pair<long long, long long>, std::vector<int>> joint;
+  for (int v = 0; v < n; v++)
+    if (T[v] || M[v]) joint[{T[v], M[v]}].push_back(v);
+  std::vector<u64> mT, mM;
+  std::vector<long long> kT, kM;
+  const bool okT = weight_classes(T, n, Wp, mT, kT), okM = weight_classes(M, n, Wp, mM, kM);
+  // separate form, merging classes with identical masks
+  std::vector<std::vector<u64>> sm;
+  std::vector<std::pair<long long, long long>> sc;
+  auto add = [&](const u64* m, long long ct, long long cm) {
+    for (size_t q = 0; q < sm.size(); q++)
+      if (std::equal(sm[q].begin(), sm[q].end(), m)) {
+        sc[q].first += ct;
+        sc[q].second += cm;
+        return;
+      }
+    sm.emplace_back(m, m + Wp);
+    sc.push_back({ct, cm});
+  };
+  if (okT && okM) {
+    for (size_t c = 0; c < kT.size(); c++) add(mT.data() + c * Wp, kT[c], 0);
+    for (size_t c = 0; c < kM.size(); c++) add(mM.data() + c * Wp, 0, kM[c]);
+  }
+  cls.clear();
+  coef.clear();
+  const bool use_joint = (int)joint.size() <= kMaxClasses &&
+                         (!(okT && okM) || joint.size() <= sm.size());
+  if (use_joint) {
+    for (auto& kv : joint) {
+      std::vector<u64> m(Wp, 0);
+      for (int v : kv.second) m[v >> 6] |= 1ull << (v & 63);
+      cls.insert(cls.end(), m.begin(), m.end());
+      coef.push_back(kv.first.first);
+      coef.push_back(kv.first.second);
+    }
+    return true;
+  }
+  if (!(okT && okM) || (int)sm.size() > kMaxClasses) return false;
+  for (size_t q = 0; q < sm.size(); q++) {
+    cls.insert(cls.end(), sm[q].begin(), sm[q].end());
+    coef.push_back(sc[q].first);
+    coef.push_back(sc[q].second);
+  }
+  return true;
+}
+
 static int upload(DevBuf<u64>& d, const std::vector<u64>& h, cudaStream_t s) {
   int rc = d.ensure(h.size());
   if (rc < 0) return rc;
@@ -191,17 +244,13 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
     }
   g->hT.assign(compute_costs, compute_costs + n);
   g->hM.assign(memory_costs, memory_costs + n);
-  std::vector<u64> cT, cM;
-  std::vector<long long> kT, kM;
-  bool okT = weight_classes(g->hT, n, Wp, cT, kT);
-  bool okM = weight_classes(g->hM, n, Wp, cM, kM);
-  g->cls_enabled = okT && okM;
-  g->KT = (int)kT.size();
-  g->KM = (int)kM.size();
+  std::vector<u64> cls;
+  std::vector<long long> coef;
+  g->cls_enabled = joint_classes(g->hT, g->hM, n, Wp, cls, coef);
+  g->K = (int)coef.size() / 2;
   if ((rc = upload(g->preds, hp, g->stream)) < 0 || (rc = upload(g->succs, hs, g->stream)) < 0 ||
       (rc = upload(g->T, g->hT, g->stream)) < 0 || (rc = upload(g->M, g->hM, g->stream)) < 0 ||
-      (rc = upload(g->clsT, cT, g->stream)) < 0 || (rc = upload(g->clsM, cM, g->stream)) < 0 ||
-      (rc = upload(g->coefT, kT, g->stream)) < 0 || (rc = upload(g->coefM, kM, g->stream)) < 0)
+      (rc = upload(g->cls, cls, g->stream)) < 0 || (rc = upload(g->coef, coef, g->stream)) < 0)
     return cleanup(rc);
   if (cudaStreamSynchronize(g->stream) != cudaSuccess)
     return cleanup(fail(REMAT_ERR_CUDA, "graph upload failed"));

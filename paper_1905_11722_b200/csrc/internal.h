@@ -116,11 +116,9 @@ struct FamilyView {
 
 struct ClassView {
   int enabled;                    // 0 -> class path unavailable (> kMaxClasses)
-  int KT, KM;
-  const u64* clsT;                // [KT][Wp]
-  const u64* clsM;                // [KM][Wp]
-  const long long* coefT;         // [KT]
-  const long long* coefM;         // [KM]
+  int K;                          // classes: T(X) = Σ_c coef[c][0]·popc(X ∩ cls_c),
+  const u64* cls;                 // [K][Wp]  M(X) = Σ_c coef[c][1]·popc(X ∩ cls_c)
+  const long long* coef;          // [K][2]
 };
 
 struct DpView {
@@ -189,9 +187,9 @@ struct remat_graph_s {
   remat::DevBuf<u64> preds, succs;
   remat::DevBuf<long long> T, M;
   // weight classes for the popcount form of T(X) / M(X)
-  int cls_enabled = 0, KT = 0, KM = 0;
-  remat::DevBuf<u64> clsT, clsM;
-  remat::DevBuf<long long> coefT, coefM;
+  int cls_enabled = 0, K = 0;
+  remat::DevBuf<u64> cls;
+  remat::DevBuf<long long> coef;
   std::vector<long long> hT, hM;
   // evaluate / simulate scratch
   remat::DevBuf<u64> chain_buf, bound_buf, cached_buf;
@@ -207,7 +205,7 @@ struct remat_graph_s {
     return remat::GraphView{n, Wp, preds.p, succs.p, T.p, M.p};
   }
   remat::ClassView classes() const {
-    return remat::ClassView{cls_enabled, KT, KM, clsT.p, clsM.p, coefT.p, coefM.p};
+    return remat::ClassView{cls_enabled, K, cls.p, coef.p};
   }
 };
 

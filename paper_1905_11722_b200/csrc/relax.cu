@@ -128,7 +128,7 @@ struct TileArgs {
   void* grow;       // [nb][rows_pb][R] global rows (split / oversized levels)
   unsigned* ctr;    // [nb][tiles] next predecessor chunk of the tile (zeroed per level)
   int tiles;
-  int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_tacc, off_pairs, off_q, off_qs, off_rows;
+  int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_coef, off_tacc, off_pairs, off_q, off_qs, off_rows;
   int bytes;
 };
 
@@ -151,6 +151,7 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   a.off_tc = take(TJ * 4 * 8);
   a.off_tcls = take(TJ * 4);
   a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
+  a.off_coef = take(cls ? 2 * K * 8 : 0);
   a.off_tacc = take(TJ * 2 * 8);
   a.off_pairs = take(kWarps * 32 * TJ * 2);
   a.off_q = take(kWarps * 32 * TJ * (int)sizeof(typename Traits<NARROW>::Q));
@@ -336,6 +337,7 @@ __global__ void __launch_bounds__(kThreads)
   long long* tc = reinterpret_cast<long long*>(sm + ta.off_tc);  // [TJ][4]
   int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);     // [TJ]
   u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
+  long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);  // [K][2]
   u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
   unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
   Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * 32 * TJ;  // feasible pairs of a chunk
@@ -364,13 +366,13 @@ __global__ void __launch_bounds__(kThreads)
   if (srow)
     for (int t = tid; t < ntj * R; t += kThreads) rows[t] = INF;
   __syncthreads();
-  const int KT = cv.KT, K = cv.KT + cv.KM;
+  const int K = cv.K;
   if (ta.cls) {
     for (int e = tid; e < ntj * K * W; e += kThreads) {
       const int jt = e / (K * W), r = e - jt * K * W, c = r / W, w = r - c * W;
-      const u64 cls = c < KT ? cv.clsT[c * W + w] : cv.clsM[(c - KT) * W + w];
-      bjc[e] = tB[jt * W + w] & cls;
+      bjc[e] = tB[jt * W + w] & cv.cls[c * W + w];
     }
+    for (int e = tid; e < 2 * K; e += kThreads) tcoef[e] = cv.coef[e];
   }
   for (int jt = tid; jt < ntj; jt += kThreads) {
     int bc = 0;
@@ -405,8 +407,8 @@ __global__ void __launch_bounds__(kThreads)
         int pc = 0;
 #pragma unroll
         for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[cc * W + w]);
-        if (cc < KT) ts += __ldg(cv.coefT + cc) * pc;
-        else ms += __ldg(cv.coefM + cc - KT) * pc;
+        ts += tcoef[2 * cc] * pc;
+        ms += tcoef[2 * cc + 1] * pc;
       }
     } else {
 #pragma unroll
@@ -859,7 +861,7 @@ static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   const FamilyView fv = f->view();
   const GraphView gv = g->view();
   const ClassView cv = g->classes();
-  const int K = cv.KT + cv.KM;
+  const int K = cv.K;
   static int num_sms = 0;
   if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
   const long long target_ctas = (long long)num_sms * 4;  // resident CTAs at 256 threads
