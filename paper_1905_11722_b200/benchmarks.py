@@ -326,3 +326,101 @@ def named_graph(name: str, **kw) -> ComputationGraph:
             )
         )
     raise ValueError(f"unknown named shape {name!r}; expected one of {NAMED_SHAPES}")
+
+
+# ---------------------------------------------------------------------------
+# Chen et al. sqrt(n) segmentation baseline (reference benchmarks.py:136-222)
+# ---------------------------------------------------------------------------
+
+
+def articulation_points(g: ComputationGraph) -> list[int]:
+    """Cut vertices of the undirected skeleton of ``g``, ascending
+    (reference benchmarks.py:136-183).  Iterative low-link DFS."""
+    n = g.n
+    nbrs = []
+    for v in range(n):
+        m = g.preds[v] | g.succs[v]
+        lst = []
+        while m:
+            low_bit = m & -m
+            lst.append(low_bit.bit_length() - 1)
+            m ^= low_bit
+        nbrs.append(lst)
+    order = [-1] * n
+    low = [0] * n
+    cut = set()
+    clock = 0
+    for root in range(n):
+        if order[root] >= 0:
+            continue
+        order[root] = low[root] = clock
+        clock += 1
+        kids = 0
+        stack = [(root, -1, iter(nbrs[root]))]
+        while stack:
+            v, up, it = stack[-1]
+            for w in it:
+                if w == up:
+                    continue
+                if order[w] >= 0:
+                    low[v] = min(low[v], order[w])
+                    continue
+                order[w] = low[w] = clock
+                clock += 1
+                stack.append((w, v, iter(nbrs[w])))
+                break
+            else:
+                stack.pop()
+                if stack:
+                    p = stack[-1][0]
+                    low[p] = min(low[p], low[v])
+                    if p == root:
+                        kids += 1
+                    elif low[v] >= order[p]:
+                        cut.add(p)
+        if kids > 1:
+            cut.add(root)
+    return sorted(cut)
+
+
+def chen_chain(g: ComputationGraph) -> tuple[list[int], int]:
+    """The Chen baseline's chain and its candidate count (host-only): candidate
+    cuts are articulation-point ancestor closures forming a strictly increasing
+    chain; a cut is taken once the running segment reaches isqrt(n) nodes; V
+    closes the chain (reference benchmarks.py:196-211)."""
+    from math import isqrt
+
+    from .graph import ancestors_closure
+
+    points = articulation_points(g)
+    cands, cur = [], 0
+    for v in points:
+        c = ancestors_closure(g, v)
+        if c != g.full_mask and c != cur and (cur & ~c) == 0:
+            cands.append(c)
+            cur = c
+    step = max(1, isqrt(g.n))
+    chain, last = [], 0
+    for c in cands:
+        if c.bit_count() - last >= step:
+            chain.append(c)
+            last = c.bit_count()
+    chain.append(g.full_mask)
+    return chain, len(points)
+
+
+def chen_baseline_plan(g: ComputationGraph, budget: int | None = None):
+    """sqrt(n)-segment checkpointing baseline scored with the same plan
+    machinery (reference benchmarks.py:186-222); infeasible if a given budget
+    is below its peak."""
+    from .planner import PlanResult, SearchStats
+    from .strategy import make_sequence, peak_memory
+
+    chain, npoints = chen_chain(g)
+    stats = SearchStats(states_visited=npoints)
+    seq = make_sequence(g, chain)
+    ev = peak_memory(g, seq)
+    if budget is not None and ev.peak_memory > budget:
+        return PlanResult(False, None, None, None, budget, "chen", "baseline", stats)
+    return PlanResult(True, seq, ev, ev.overhead, ev.peak_memory if budget is None else budget,
+                      "chen", "baseline", stats)

@@ -34,7 +34,9 @@ from pathlib import Path
 sys.dont_write_bytecode = True
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from remat.benchmarks import TopologySpec, generate  # noqa: E402
+from remat.benchmarks import (  # noqa: E402
+    TopologySpec, articulation_points, chen_baseline_plan, generate,
+)
 from remat.graph import graph_from_document, graph_to_document  # noqa: E402
 from remat.lattice import all_lower_sets, pruned_lower_sets  # noqa: E402
 from remat.planner import (  # noqa: E402
@@ -248,7 +250,22 @@ def reports():
             b, tc = min_feasible_budget(g, fam, "minimize")
             mc = dp_plan(PlanRequest(g, b, fam, "maximize"))
             entry["plans"].append({"family": fam, "b_min": b, "tc": plan_json(tc), "mc": plan_json(mc)})
+        chen = chen_baseline_plan(g)
+        entry["chen"] = {"points": articulation_points(g), "plan": plan_json(chen),
+                         "table": build_report(g).render_table()}
         out.append(entry)
+    # Chen baseline on more archetype shapes (benchmarks.py:136-222)
+    rng = random.Random(0xC4E)
+    for fam in ("chain", "skip-chain", "resnet-like", "densenet-like", "unet-like", "random-dag"):
+        for seed in range(4):
+            spec = TopologySpec(fam, rng.randint(3, 60), seed=seed,
+                                edge_prob=rng.choice([0.1, 0.3, 0.6]))
+            g = generate(spec)
+            out.append({"spec": {"family": fam, "depth": spec.depth, "seed": seed,
+                                 "edge_prob": spec.edge_prob, "cost_model": spec.cost_model},
+                        "graph": graph_to_document(g),
+                        "chen": {"points": articulation_points(g),
+                                 "plan": plan_json(chen_baseline_plan(g))}})
     return out
 
 

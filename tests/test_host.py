@@ -41,6 +41,19 @@ from paper_1905_11722_b200.schedule import (
 ROOT = Path(__file__).resolve().parents[1]
 
 
+def test_chen_chain_matches_reference():
+    """Articulation points and the Chen sqrt(n) chain (host-only part of
+    chen_baseline_plan, reference benchmarks.py:136-222)."""
+    from paper_1905_11722_b200 import articulation_points, chen_chain
+
+    for rec in golden("reports.json"):
+        g = load(rec["graph"])
+        assert articulation_points(g) == rec["chen"]["points"], rec["spec"]
+        chain, npts = chen_chain(g)
+        assert chain == [h(x) for x in rec["chen"]["plan"]["chain"]], rec["spec"]
+        assert npts == rec["chen"]["plan"]["stats"]["states_visited"]
+
+
 # --- graph format ------------------------------------------------------------
 
 def test_golden_graph_documents_round_trip():
