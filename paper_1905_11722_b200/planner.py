@@ -173,6 +173,78 @@ def min_feasible_budget(
         s.close()
 
 
+def dfs_exhaustive_plan(req: PlanRequest, state_cap: int = DEFAULT_DFS_STATE_CAP) -> PlanResult:
+    """Exhaustive depth-first search over every chain of the family — the
+    reference's exponential optimality oracle (planner.py:226-268), kept on the
+    host by design (n <= ~12, nothing for a GPU to do).  The
+    family comes from the device; pair constants are the reference definitions
+    (planner.py:104-131).  Raises ``SearchCapExceeded`` past ``state_cap``
+    visited states."""
+    from .graph import boundary, delta_minus, delta_plus, memory_of, time_of
+    from .lattice import all_lower_sets, pruned_lower_sets
+    from .strategy import make_sequence, peak_memory
+
+    g = req.graph
+    fam = all_lower_sets(g, req.lattice_cap) if req.family == "full" else pruned_lower_sets(g)
+    masks = list(fam.masks)
+    bound = [boundary(g, m) for m in masks]
+    base = []
+    for m in masks:
+        out = delta_plus(g, m)
+        base.append(memory_of(g, out & ~m) + memory_of(g, delta_minus(g, out) & ~m))
+    nxt = [[] for _ in masks]
+    for i, lo in enumerate(masks):
+        for j in range(i + 1, len(masks)):
+            hi = masks[j]
+            if lo & ~hi:
+                continue
+            seg = hi & ~lo
+            nxt[i].append((j, 2 * memory_of(g, seg) + base[j], time_of(g, seg & ~bound[j]),
+                           memory_of(g, bound[j] & ~lo)))
+    stats = SearchStats()
+    t0 = time.perf_counter()
+    minimize = req.objective == "minimize"
+    full = len(masks) - 1
+    best = None
+    trail: list[int] = []
+    # explicit stack: (cell, t, m, next successor position)
+    stack = [(0, 0, 0, 0)]
+    stats.states_visited = 1
+    while stack:
+        i, t, m, k = stack[-1]
+        if i == full:
+            if best is None or (t < best[0] if minimize else t > best[0]):
+                best = (t, trail.copy())
+            stack.pop()
+            if trail:
+                trail.pop()
+            continue
+        if k == len(nxt[i]):
+            stack.pop()
+            if trail:
+                trail.pop()
+            continue
+        stack[-1] = (i, t, m, k + 1)
+        j, fixed, dt, dm = nxt[i][k]
+        stats.transitions += 1
+        if m + fixed > req.budget:
+            continue
+        stats.states_visited += 1
+        if stats.states_visited > state_cap:
+            raise SearchCapExceeded(f"exhaustive search exceeded {state_cap} states")
+        trail.append(j)
+        stack.append((j, t + dt, m + dm, 0))
+    stats.wall_time_s = time.perf_counter() - t0
+    if best is None:
+        return PlanResult(False, None, None, None, req.budget, req.family, req.objective, stats)
+    t_star, path = best
+    seq = make_sequence(g, [masks[j] for j in path])
+    ev = peak_memory(g, seq)
+    if ev.overhead != t_star or ev.peak_memory > req.budget:
+        raise PlannerError("exhaustive search produced an inconsistent plan")
+    return PlanResult(True, seq, ev, t_star, req.budget, req.family, req.objective, stats)
+
+
 def memory_centric_plan(g, family: str = "full",
                         lattice_cap: int = DEFAULT_LATTICE_CAP) -> PlanResult:
     """Overhead-maximising plan at the minimal feasible budget (planner.py:300-313)."""

@@ -328,6 +328,70 @@ def named(slow: bool):
     return out
 
 
+def cli_corpus():
+    """The reference CLI's own outputs (cli.py): plan JSON (byte-stable),
+    simulate summary / trace / schedule text, report table + CSV, exit codes
+    and stderr, for a handful of graphs and flag combinations."""
+    import contextlib
+    import io
+    import tempfile
+
+    from remat.cli import main as ref_main
+
+    out = []
+    with tempfile.TemporaryDirectory() as td:
+        def run(argv):
+            so, se = io.StringIO(), io.StringIO()
+            with contextlib.redirect_stdout(so), contextlib.redirect_stderr(se):
+                code = ref_main(argv)
+            return code, so.getvalue(), se.getvalue()
+
+        graphs = {}
+        for name, gen in [("chain3", ["--family", "chain", "--depth", "3"]),
+                          ("dense4", ["--family", "densenet-like", "--depth", "4"]),
+                          ("skip9", ["--family", "skip-chain", "--depth", "9", "--skip", "3",
+                                     "--cost-model", "conv-weighted"]),
+                          ("rand8", ["--family", "random-dag", "--depth", "8", "--seed", "3",
+                                     "--edge-prob", "0.4"]),
+                          ("unet5", ["--family", "unet-like", "--depth", "5",
+                                     "--cost-model", "conv-weighted"])]:
+            path = os.path.join(td, name + ".json")
+            code, _, _ = run(["gen", *gen, "--out", path])
+            graphs[name] = (path, open(path).read())
+            out.append({"argv": ["gen", *gen], "code": code, "files": {"out": graphs[name][1]}})
+        for name, (path, text) in graphs.items():
+            for algo in ("exact", "approx", "dfs", "chen"):
+                for budget in ("min", "0", "7", "40"):
+                    for obj in ("time", "memory"):
+                        if algo == "chen" and obj == "memory":
+                            continue
+                        if algo == "dfs" and name in ("unet5", "dense4") and budget == "min":
+                            continue
+                        argv = ["plan", "--graph", "@" + name, "--budget", budget, "--algo", algo,
+                                "--objective", obj]
+                        code, so, se = run([a if a[0] != "@" else path for a in argv])
+                        out.append({"argv": argv, "code": code, "stdout": so, "stderr": se})
+            plan_path = os.path.join(td, "plan.json")
+            run(["plan", "--graph", path, "--budget", "min", "--out", plan_path])
+            plan_text = open(plan_path).read()
+            for live in ("on", "off"):
+                tr, sc = os.path.join(td, "t.json"), os.path.join(td, "s.txt")
+                code, so, se = run(["simulate", "--graph", path, "--plan", plan_path,
+                                    "--liveness", live, "--trace", tr, "--schedule", sc])
+                out.append({"argv": ["simulate", "--graph", "@" + name, "--plan", "@plan",
+                                     "--liveness", live, "--trace", "@trace", "--schedule",
+                                     "@schedule"],
+                            "plan": plan_text, "code": code, "stdout": so, "stderr": se,
+                            "files": {"trace": open(tr).read(), "schedule": open(sc).read()}})
+            csv_path = os.path.join(td, "r.csv")
+            code, so, se = run(["report", "--graph", path, "--csv", csv_path])
+            out.append({"argv": ["report", "--graph", "@" + name, "--csv", "@csv"], "code": code,
+                        "stdout": so, "stderr": se, "files": {"csv": open(csv_path).read()}})
+        for name in graphs:
+            graphs[name] = graphs[name][1]
+    return [{"graphs": graphs, "runs": out}]
+
+
 def named_xslow():
     """Reference runs that take many minutes in the build container: C5 at
     p=0.4 (F=3,293, ~440 s of TransitionIndex) and memory-centric U-Net."""
@@ -367,6 +431,7 @@ def main() -> None:
         "sim_corpus.json": sim_corpus,
         "reports.json": reports,
         "named.json": lambda: named(slow),
+        "cli.json": cli_corpus,
     }
     if "--xslow" in sys.argv:
         jobs = {"named_xslow.json": named_xslow}
