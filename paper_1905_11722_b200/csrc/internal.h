@@ -226,7 +226,9 @@ struct remat_family_s {
   remat::DevBuf<int> parent, flen, ccount;
   remat::DevBuf<long long> mmin, budgets, results;
   remat::DevBuf<u64> trans, npairs;
-  remat::DevBuf<unsigned> ctr;                  // per-tile chunk counters
+  remat::DevBuf<unsigned> ctr;                  // per-tile chunk + done counters (zero)
+  size_t ctr_cap = 0, grow_cap = 0;             // capacities of ctr / rowscratch (INF rows)
+  int grow_key = 0;                             // key size rowscratch was filled for
   remat::DevBuf<u64> rowscratch, chain_out, cached_out;
   remat::DevBuf<long long> stage_out, terms;
   remat::DevBuf<int> chain_idx;

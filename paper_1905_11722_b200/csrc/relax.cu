@@ -246,9 +246,15 @@ __device__ __forceinline__ T warp_incl_min(T v) {
 // K5 for one finished row (one warp): |cell|, the strict prefix-min frontier in
 // t order (ascending for minimize, descending for maximize; planner.py:153-161)
 // compacted into the member's frontier slot with its back-pointers.
+template <typename Key>
+__device__ __forceinline__ Key row_ld(const Key* p, bool global) {
+  return global ? __ldcg(p) : *p;  // global rows: L2 (other SMs' atomics land there)
+}
+
 template <bool NARROW>
 __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int Rj,
-                                  const DpView& dp, const FamilyView& fv, long long j, int b) {
+                                  const DpView& dp, const FamilyView& fv, long long j, int b,
+                                  bool global = false) {
   using Key = typename Traits<NARROW>::Key;
   using E = typename Traits<NARROW>::E;
   constexpr Key INF = Traits<NARROW>::INF;
@@ -261,7 +267,7 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
   Key lmin = INF;
   int cells = 0;
   for (int s = s0; s < s1; s++) {
-    Key key = row[mx ? Rj - 1 - s : s];
+    Key key = row_ld(row + (mx ? Rj - 1 - s : s), global);
     if (key != INF) {
       cells++;
       Key m = key >> IB;
@@ -274,7 +280,7 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
   int nf = 0;
   Key run = pm;
   for (int s = s0; s < s1; s++) {
-    Key key = row[mx ? Rj - 1 - s : s];
+    Key key = row_ld(row + (mx ? Rj - 1 - s : s), global);
     if (key != INF && (key >> IB) < run) {
       nf++;
       run = key >> IB;
@@ -291,7 +297,7 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
   const Key pmask = (Key(1) << IB) - 1;
   for (int s = s0; s < s1; s++) {
     const int t = mx ? Rj - 1 - s : s;
-    Key key = row[t];
+    Key key = row_ld(row + t, global);
     if (key != INF && (key >> IB) < run) {
       run = key >> IB;
       E e{};
@@ -626,10 +632,12 @@ __global__ void __launch_bounds__(kThreads)
     if (tacc[tid * 2 + 1])
       atomicAdd(reinterpret_cast<unsigned long long*>(dp.npairs + at), tacc[tid * 2 + 1]);
   }
+  unsigned* done = ctr + (size_t)gridDim.y * ta.tiles;  // finished CTAs of the tile
   if (splits == 1 && srow) {
     for (int jt = warp; jt < ntj; jt += kWarps)
       finalize_row_warp<NARROW>(rows + jt * R, (int)(fv.TL[j0 + jt] + 1), dp,
                                 fv, j0 + jt, b);
+    if (tid == 0) *ctr = 0;  // counters are self-resetting for the next level
     return;
   }
   if (srow && s_worked)  // fold this CTA's rows into the tile's global rows
@@ -637,19 +645,25 @@ __global__ void __launch_bounds__(kThreads)
       const Key key = rows[t];
       if (key != INF) atomicMin(grow_t + t, key);
     }
-}
-
-// K5 for split / global-row levels: one warp per (target, budget).
-template <bool NARROW>
-__global__ void __launch_bounds__(kThreads)
-    k_finalize_rows(FamilyView fv, DpView dp, long long jbase, int width, int rows_pb, int R,
-                    const void* __restrict__ grow) {
-  using Key = typename Traits<NARROW>::Key;
-  const int tj = blockIdx.x * kWarps + (threadIdx.x >> 5), b = blockIdx.y;
-  if (tj >= width) return;
-  const long long j = jbase + tj;
-  const Key* row = reinterpret_cast<const Key*>(grow) + ((size_t)b * rows_pb + tj) * R;
-  finalize_row_warp<NARROW>(row, (int)(fv.TL[j] + 1), dp, fv, j, b);
+  // the last CTA of the tile to finish finalizes its rows from L2 and leaves
+  // rows and counters as it found them (INF / 0), so no per-level fill,
+  // memset or finalize launch is needed
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_worked = atomicAdd(done, 1u) == (unsigned)(splits - 1);
+  __syncthreads();
+  if (!s_worked) return;
+  __threadfence();
+  for (int jt = warp; jt < ntj; jt += kWarps) {
+    const int Rj = (int)(fv.TL[j0 + jt] + 1);
+    finalize_row_warp<NARROW>(grow_t + (size_t)jt * R, Rj, dp, fv, j0 + jt, b, true);
+    __syncwarp();
+    for (int t = lane; t < Rj; t += 32) grow_t[(size_t)jt * R + t] = INF;
+  }
+  if (tid == 0) {
+    *ctr = 0;
+    *done = 0;
+  }
 }
 
 template <typename Key>
@@ -847,6 +861,29 @@ static int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int
   RM_CUDA(cudaMemsetAsync(f->ccount.p, 0, sizeof(int) * nb * F, s));
   k_dp_init<NARROW><<<(nb + 127) / 128, 128, 0, s>>>(f->dp_view(), F, nb);
   RM_LAUNCHED();
+  // per-level scratch for the widest level: tile counters (zero) and global
+  // rows (INF); the relaxation kernels leave both as they found them
+  using Key = typename Traits<NARROW>::Key;
+  long long wmax = 1, rmax = 1;
+  for (int l = 1; l <= n; l++) {
+    wmax = std::max(wmax, f->level_start[l + 1] - f->level_start[l]);
+    rmax = std::max(rmax, f->level_maxR[l]);
+  }
+  const size_t need_ctr = (size_t)2 * nb * wmax;
+  const size_t need_rows = (size_t)nb * (wmax + kMaxTJ) * rmax;
+  if (need_ctr > f->ctr_cap) {
+    if ((rc = f->ctr.ensure(need_ctr)) < 0) return rc;
+    f->ctr_cap = need_ctr;
+    RM_CUDA(cudaMemsetAsync(f->ctr.p, 0, sizeof(unsigned) * need_ctr, s));
+  }
+  if (need_rows > f->grow_cap || f->grow_key != (int)sizeof(Key)) {
+    if ((rc = f->rowscratch.ensure((need_rows * sizeof(Key) + 7) / 8)) < 0) return rc;
+    f->grow_cap = need_rows;
+    f->grow_key = (int)sizeof(Key);
+    k_fill<Key><<<(unsigned)std::min<size_t>((need_rows + 255) / 256, 4096), 256, 0, s>>>(
+        reinterpret_cast<Key*>(f->rowscratch.p), need_rows, Traits<NARROW>::INF);
+    RM_LAUNCHED();
+  }
   return REMAT_OK;
 }
 
@@ -892,26 +929,18 @@ static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   ta.grow = nullptr;
   ta.rows_pb = (int)(tiles * TJ);
   ta.tiles = (int)tiles;
-  if ((rc = f->ctr.ensure((size_t)nb * tiles)) < 0) return rc;
-  ta.ctr = f->ctr.p;
-  RM_CUDA(cudaMemsetAsync(ta.ctr, 0, sizeof(unsigned) * nb * tiles, s));
+  ta.ctr = f->ctr.p;  // [nb][tiles] chunk counters + [nb][tiles] done counters, all zero
+  if ((size_t)2 * nb * tiles > f->ctr_cap)
+    return fail(REMAT_ERR_INTERNAL, "tile counter capacity exceeded");
   if (splits > 1 || !ta.smem_rows) {
     const size_t cells = (size_t)nb * tiles * TJ * R;
-    if ((rc = f->rowscratch.ensure((cells * sizeof(Key) + 7) / 8)) < 0) return rc;
-    ta.grow = f->rowscratch.p;
-    k_fill<Key><<<(unsigned)std::min<size_t>((cells + 255) / 256, 4096), 256, 0, s>>>(
-        reinterpret_cast<Key*>(ta.grow), cells, Traits<NARROW>::INF);
-    RM_LAUNCHED();
+    if (cells > f->grow_cap) return fail(REMAT_ERR_INTERNAL, "row scratch capacity exceeded");
+    ta.grow = f->rowscratch.p;  // all INF between levels
   }
   k_relax_tile<W, NARROW><<<dim3((unsigned)(tiles * splits), (unsigned)nb), kThreads, ta.bytes,
                             s>>>(fv, gv, cv, dp, ta);
   RM_LAUNCHED();
   f->relax_launches++;
-  if (ta.grow) {
-    k_finalize_rows<NARROW><<<dim3((unsigned)((width + kWarps - 1) / kWarps), (unsigned)nb),
-                              kThreads, 0, s>>>(fv, dp, lo, (int)width, ta.rows_pb, R, ta.grow);
-    RM_LAUNCHED();
-  }
   return REMAT_OK;
 }
 
