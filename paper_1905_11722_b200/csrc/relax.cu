@@ -439,11 +439,16 @@ __global__ void __launch_bounds__(kThreads)
     return cap >= mmi;
   };
 
-  while (true) {
+  // the first chunk of every warp is static (CTA rank within the tile x warps
+  // + warp), later ones come from the counter, offset past the static ones
+  const long long nstatic = (long long)splits * kWarps;
+  auto next_chunk = [&]() {
     unsigned got = 0;
     if (lane == 0) got = atomicAdd(ctr, 1u);
-    const long long ch = __shfl_sync(kFull, got, 0);
-    if (ch >= nch) break;
+    return nstatic + (long long)__shfl_sync(kFull, got, 0);
+  };
+  for (long long ch = (long long)(blockIdx.x - tile * splits) * kWarps + warp; ch < nch;
+       ch = next_chunk()) {
     worked = true;
     // lane = predecessor i: its set and scalars in one round of loads
     const long long i = ch * 32 + lane;
