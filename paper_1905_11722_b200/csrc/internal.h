@@ -227,6 +227,7 @@ struct remat_family_s {
   remat::DevBuf<long long> mmin, budgets, results;
   remat::DevBuf<u64> trans, npairs;
   remat::DevBuf<unsigned> ctr;                  // per-tile chunk + done counters (zero)
+  remat::DevBuf<unsigned char> levelargs;       // TileArgs of a batched level run
   size_t ctr_cap = 0, grow_cap = 0;             // capacities of ctr / rowscratch (INF rows)
   int grow_key = 0;                             // key size rowscratch was filled for
   remat::DevBuf<u64> rowscratch, chain_out, cached_out;
@@ -258,6 +259,7 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 // level), finish; solve_batch runs all levels on one device
 int solve_begin(remat_family_s* f, const std::vector<long long>& budgets, int objective);
 int solve_level(remat_family_s* f, int lvl, long long lo, long long hi);
+int solve_levels(remat_family_s* f, const std::vector<int>& lvls);  // full ranges, batched
 int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                  long long* stage_memory);
 int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,

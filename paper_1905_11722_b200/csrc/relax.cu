@@ -39,6 +39,8 @@
 // with Σ_i|frontier_i| and the comparable-pair counts accumulated during the
 // scan these are exactly table_entries, states_visited and transitions
 // (Appendix A.3).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <climits>
 
@@ -317,24 +319,26 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
   }
 }
 
-// K4 (+K5 when the tile is not split).  Grid: (tiles·splits, nb).
+// K4 (+K5): one (tile, split) "virtual CTA" `vbx` of budget b.  Run either as
+// one CTA of k_relax_tile (grid (tiles·splits, nb)) or inside the persistent
+// k_relax_levels loop.
 template <int W, bool NARROW>
-__global__ void __launch_bounds__(kThreads)
-    k_relax_tile(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
+__device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView& g,
+                                           const ClassView& cv, const DpView& dp,
+                                           const TileArgs& ta, const int vbx, const int b,
+                                           const int nb, unsigned char* sm) {
   using Key = typename Traits<NARROW>::Key;
   using E = typename Traits<NARROW>::E;
   using Q = typename Traits<NARROW>::Q;
   using MT = typename Traits<NARROW>::M;
   constexpr Key INF = Traits<NARROW>::INF;
-  extern __shared__ __align__(16) unsigned char sm[];
   __shared__ int s_worked;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1;
   const int TJ = ta.TJ, R = ta.R, splits = ta.splits;
   if (tid == 0) s_worked = 0;
   const long long F = fv.F;
-  const int tile = blockIdx.x / splits;
-  const int b = blockIdx.y;
+  const int tile = vbx / splits;
   const long long j0 = ta.jbase + (long long)tile * TJ;
   const int ntj = (int)min((long long)TJ, ta.jbase + ta.width - j0);
 
@@ -447,7 +451,7 @@ __global__ void __launch_bounds__(kThreads)
     if (lane == 0) got = atomicAdd(ctr, 1u);
     return nstatic + (long long)__shfl_sync(kFull, got, 0);
   };
-  for (long long ch = (long long)(blockIdx.x - tile * splits) * kWarps + warp; ch < nch;
+  for (long long ch = (long long)(vbx - tile * splits) * kWarps + warp; ch < nch;
        ch = next_chunk()) {
     worked = true;
     // lane = predecessor i: its set and scalars in one round of loads
@@ -637,7 +641,7 @@ __global__ void __launch_bounds__(kThreads)
     if (tacc[tid * 2 + 1])
       atomicAdd(reinterpret_cast<unsigned long long*>(dp.npairs + at), tacc[tid * 2 + 1]);
   }
-  unsigned* done = ctr + (size_t)gridDim.y * ta.tiles;  // finished CTAs of the tile
+  unsigned* done = ctr + (size_t)nb * ta.tiles;  // finished CTAs of the tile
   if (splits == 1 && srow) {
     for (int jt = warp; jt < ntj; jt += kWarps)
       finalize_row_warp<NARROW>(rows + jt * R, (int)(fv.TL[j0 + jt] + 1), dp,
@@ -668,6 +672,36 @@ __global__ void __launch_bounds__(kThreads)
   if (tid == 0) {
     *ctr = 0;
     *done = 0;
+  }
+}
+
+template <int W, bool NARROW>
+__global__ void __launch_bounds__(kThreads)
+    k_relax_tile(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  relax_body<W, NARROW>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
+}
+
+// Several consecutive small levels in ONE cooperative launch: every block
+// walks the (tile, split, budget) virtual CTAs of a level, then a grid barrier
+// publishes the level (its tiles were finalized by their last CTA) before the
+// next one starts.  Removes the launch + ramp of each of the hundreds of
+// narrow levels of deep lattices (C5: 516 levels).
+template <int W, bool NARROW>
+__global__ void __launch_bounds__(kThreads)
+    k_relax_levels(FamilyView fv, GraphView g, ClassView cv, DpView dp,
+                   const TileArgs* __restrict__ levels, int nlev, int nb) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char sm[];
+  for (int l = 0; l < nlev; l++) {
+    const TileArgs ta = levels[l];
+    const int per = ta.tiles * ta.splits;
+    for (int v = blockIdx.x; v < per * nb; v += gridDim.x) {
+      relax_body<W, NARROW>(fv, g, cv, dp, ta, v % per, v / per, nb, sm);
+      __syncthreads();
+    }
+    grid.sync();
   }
 }
 
@@ -817,6 +851,10 @@ __global__ void k_reconstruct(FamilyView fv, GraphView g, DpView dp, int n,
 
 static constexpr int kSmemLimit = 200 * 1024;  // dynamic shared bytes per CTA
 static constexpr int kRowBudget = 64 * 1024;   // tile rows per CTA (4 CTAs/SM)
+// levels with at most this many (target, predecessor) subset tests are batched
+// into one cooperative launch (their work is a fraction of one GPU wave)
+static constexpr long long kSmallLevelTests = 4LL << 20;
+static constexpr long long kSmallLevelPreds = 32LL << 10;
 
 // The solve in three phases so the level loop can be driven from outside
 // (level sharding, shard.cu): begin (buffers + the empty set), one call per
@@ -893,7 +931,8 @@ static int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int
 }
 
 template <int W, bool NARROW>
-static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
+static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArgs& ta,
+                        long long max_vctas = 0) {
   using Key = typename Traits<NARROW>::Key;
   remat_graph_s* g = f->g;
   cudaStream_t s = g->stream;
@@ -909,7 +948,6 @@ static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   const long long target_ctas = (long long)num_sms * 4;  // resident CTAs at 256 threads
   const long long j0 = f->level_start[lvl];               // predecessors: [0, j0)
   const long long width = hi - lo;
-  if (width <= 0) return REMAT_OK;
   const int R = (int)f->level_maxR[lvl];
   // targets per tile: as many rows as fit the per-CTA row budget, <= width
   int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ, width),
@@ -920,12 +958,13 @@ static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   const long long want = (long long)num_sms * 64;
   while (TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
   const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
-  TileArgs ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
+  ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
   if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
   const long long tiles = (width + TJ - 1) / TJ;
   // split the predecessor scan across CTAs when the level alone cannot fill
   // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
   long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
+  if (max_vctas > 0) splits = max_vctas / (tiles * nb);  // persistent: one round per block
   splits = std::max(1LL, std::min(splits, nch / kWarps));
   ta.jbase = lo;
   ta.pend = j0;
@@ -942,8 +981,80 @@ static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
     if (cells > f->grow_cap) return fail(REMAT_ERR_INTERNAL, "row scratch capacity exceeded");
     ta.grow = f->rowscratch.p;  // all INF between levels
   }
-  k_relax_tile<W, NARROW><<<dim3((unsigned)(tiles * splits), (unsigned)nb), kThreads, ta.bytes,
-                            s>>>(fv, gv, cv, dp, ta);
+  return REMAT_OK;
+}
+
+template <int W, bool NARROW>
+static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
+  TileArgs ta;
+  if (hi <= lo) return REMAT_OK;
+  int rc = plan_level_w<W, NARROW>(f, lvl, lo, hi, ta);
+  if (rc < 0) return rc;
+  k_relax_tile<W, NARROW><<<dim3((unsigned)(ta.tiles * ta.splits), (unsigned)f->cur_nb), kThreads,
+                            ta.bytes, f->g->stream>>>(f->view(), f->g->view(), f->g->classes(),
+                                                      f->dp_view(), ta);
+  RM_LAUNCHED();
+  f->relax_launches++;
+  return REMAT_OK;
+}
+
+// A run of consecutive small levels (full target ranges) as one cooperative
+// k_relax_levels launch.
+template <int W, bool NARROW>
+static int levels_w(remat_family_s* f, const std::vector<int>& lvls) {
+  std::vector<TileArgs> tas(lvls.size());
+  int maxbytes = 0, rc;
+  static int attr_bytes = -1;
+  if (attr_bytes < 0) {
+    RM_CUDA(cudaFuncSetAttribute(k_relax_levels<W, NARROW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    attr_bytes = kSmemLimit;
+  }
+  static int num_sms0 = 0;
+  if (!num_sms0)
+    RM_CUDA(cudaDeviceGetAttribute(&num_sms0, cudaDevAttrMultiProcessorCount, f->g->device));
+  // size the grid from a first plan, then re-plan every level for one round
+  for (int pass = 0; pass < 2; pass++) {
+    long long grid = 0;
+    if (pass == 1) {
+      int b0 = 0;
+      RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, k_relax_levels<W, NARROW>,
+                                                            kThreads, maxbytes));
+      grid = (long long)num_sms0 * std::min(std::max(b0, 1), 4);
+    }
+    maxbytes = 0;
+    for (size_t k = 0; k < lvls.size(); k++) {
+      const int l = lvls[k];
+      if ((rc = plan_level_w<W, NARROW>(f, l, f->level_start[l], f->level_start[l + 1], tas[k],
+                                        grid)) < 0)
+        return rc;
+      maxbytes = std::max(maxbytes, tas[k].bytes);
+    }
+  }
+  int bps = 0;
+  RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_relax_levels<W, NARROW>, kThreads,
+                                                        maxbytes));
+  if (bps < 1) {  // cannot be co-resident: per-level launches instead
+    for (int l : lvls)
+      if ((rc = level_w<W, NARROW>(f, l, f->level_start[l], f->level_start[l + 1])) < 0) return rc;
+    return REMAT_OK;
+  }
+  static int num_sms = 0;
+  if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, f->g->device));
+  cudaStream_t s = f->g->stream;
+  if ((rc = f->levelargs.ensure(tas.size() * sizeof(TileArgs))) < 0) return rc;
+  RM_CUDA(cudaMemcpyAsync(f->levelargs.p, tas.data(), tas.size() * sizeof(TileArgs),
+                          cudaMemcpyHostToDevice, s));
+  FamilyView fv = f->view();
+  GraphView gv = f->g->view();
+  ClassView cv = f->g->classes();
+  DpView dp = f->dp_view();
+  const TileArgs* la = reinterpret_cast<const TileArgs*>(f->levelargs.p);
+  int nl = (int)tas.size(), nb = f->cur_nb;
+  void* args[] = {&fv, &gv, &cv, &dp, (void*)&la, &nl, &nb};
+  RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_relax_levels<W, NARROW>,
+                                      dim3((unsigned)(num_sms * std::min(bps, 4))), dim3(kThreads),
+                                      args, (size_t)maxbytes, s));
   RM_LAUNCHED();
   f->relax_launches++;
   return REMAT_OK;
@@ -1061,6 +1172,12 @@ int solve_level(remat_family_s* f, int lvl, long long lo, long long hi) {
   });
 }
 
+int solve_levels(remat_family_s* f, const std::vector<int>& lvls) {
+  return dispatch_solve(f, f->cur_narrow, [&](auto wc, auto nc) {
+    return levels_w<decltype(wc)::value, decltype(nc)::value>(f, lvls);
+  });
+}
+
 int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                  long long* stage_memory) {
   return dispatch_solve(f, f->cur_narrow, [&](auto wc, auto nc) {
@@ -1074,10 +1191,31 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
                 long long* stage_memory) {
   int rc = solve_begin(f, budgets, objective);
   if (rc < 0) return rc;
+  // levels whose subset tests fit one wave of the GPU run back to back in a
+  // single cooperative launch; wide levels get their own launch
+  std::vector<int> run;
+  auto flush = [&]() {
+    int r = REMAT_OK;
+    if (run.size() == 1)
+      r = solve_level(f, run[0], f->level_start[run[0]], f->level_start[run[0] + 1]);
+    else if (!run.empty())
+      r = solve_levels(f, run);
+    run.clear();
+    return r;
+  };
   for (int lvl = 1; lvl <= f->g->n; lvl++) {
-    rc = solve_level(f, lvl, f->level_start[lvl], f->level_start[lvl + 1]);
-    if (rc < 0) return rc;
+    const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
+    if (w == 0) continue;
+    // (a narrow level over a long predecessor range can still carry many
+    // frontier entries per pair: those keep their own launch)
+    if (w * j0 * (long long)budgets.size() <= kSmallLevelTests && j0 <= kSmallLevelPreds) {
+      run.push_back(lvl);
+      continue;
+    }
+    if ((rc = flush()) < 0) return rc;
+    if ((rc = solve_level(f, lvl, j0, j0 + w)) < 0) return rc;
   }
+  if ((rc = flush()) < 0) return rc;
   return solve_finish(f, info, chain_masks, cached_masks, stage_memory);
 }
 
