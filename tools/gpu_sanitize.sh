@@ -1,0 +1,22 @@
+#!/bin/bash
+# compute-sanitizer memcheck + racecheck on small exact-DP solves (both key widths)
+mkdir -p gpurun_out
+cat > /tmp/san.py <<'PY'
+import os, sys
+sys.path.insert(0, os.getcwd())
+from paper_1905_11722_b200 import named_graph, Solver, dp_plan, PlanRequest
+from paper_1905_11722_b200.shard import loopback_plans
+g = named_graph("unet", skip_len=2)
+s = Solver(g, "full")
+print(s.plans([2 * g.total_memory, 200]), flush=True)
+print(s.min_feasible_budget("maximize")[0])
+s.close()
+g = named_graph("random-dag", depth=64, edge_prob=0.4, seed=0)
+print(dp_plan(PlanRequest(g, 2 * g.total_memory, "full")).objective_value)
+print(loopback_plans(g, [100], 3)[0].objective_value)
+PY
+timeout 1200 compute-sanitizer --tool memcheck --leak-check no python /tmp/san.py > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/memcheck.log
+REMAT_FORCE_WIDE=1 timeout 1200 compute-sanitizer --tool memcheck python /tmp/san.py > gpurun_out/memcheck_wide.log 2>&1; echo "rc=$?" >> gpurun_out/memcheck_wide.log
+timeout 1800 compute-sanitizer --tool racecheck python /tmp/san.py > gpurun_out/racecheck.log 2>&1; echo "racecheck rc=$?" >> gpurun_out/racecheck.log
+timeout 1200 compute-sanitizer --tool synccheck python /tmp/san.py > gpurun_out/synccheck.log 2>&1; echo "synccheck rc=$?" >> gpurun_out/synccheck.log
+tail -3 gpurun_out/memcheck.log gpurun_out/memcheck_wide.log gpurun_out/racecheck.log gpurun_out/synccheck.log
