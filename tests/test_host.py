@@ -235,3 +235,29 @@ def test_no_oracle_import_in_product_package():
     pkg = ROOT / "paper_1905_11722_b200"
     for p in pkg.rglob("*.py"):
         assert not re.search(r"^\s*(from|import)\s+oracle", p.read_text(), re.M), p
+
+
+# --- C-ABI argument validation (runs before any device work) -------------------
+
+def _raw_graph(n, tcost=1, mcost=1):
+    import numpy as np
+
+    from paper_1905_11722_b200.graph import graph_from_document
+
+    doc = {"nodes": [{"id": f"v{i}", "compute_cost": tcost, "memory_cost": mcost}
+                     for i in range(n)],
+           "edges": [[f"v{i}", f"v{i + 1}"] for i in range(n - 1)]}
+    return graph_from_document(doc)
+
+
+def test_graph_size_limits_are_reported_not_crashed():
+    from paper_1905_11722_b200._native import DeviceGraph
+    from paper_1905_11722_b200.graph import GraphError
+
+    with pytest.raises(ValueError, match="above 1024 nodes"):
+        DeviceGraph(_raw_graph(1025))
+    # dense overhead rows: T(V) must stay below 2^24
+    with pytest.raises(GraphError, match="dense overhead-row limit"):
+        DeviceGraph(_raw_graph(4, tcost=1 << 23))
+    with pytest.raises(GraphError, match="below 2\\^61"):
+        DeviceGraph(_raw_graph(4, mcost=1 << 60))
