@@ -138,9 +138,13 @@ def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or (args.parallel == "levels" and args.impl == "ours"):
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         backend = "nccl" if args.impl == "ours" else "gloo"
         if backend == "nccl":
             import torch
@@ -238,16 +242,15 @@ def run_ours(args, world, rank, local):
     from paper_1905_11722_b200._native import DeviceFamily, DeviceGraph, kernel_launches
 
     g, name = workload(args)
-    levels = world > 1 and args.parallel == "levels"
+    levels = args.parallel == "levels"
     if levels:
         # level sharding: every rank works on the SAME solve (budget 2·M(V));
         # each level's targets are split over the ranks, one NCCL all-gather
         # per level (paper_1905_11722_b200/shard.py)
-        from paper_1905_11722_b200._native import Comm
-        from paper_1905_11722_b200.shard import exchange_unique_id
+        from paper_1905_11722_b200.shard import communicator
 
         budget = 2 * g.total_memory
-        comm = Comm(exchange_unique_id(), world, rank, local)
+        comm = communicator(local)
     else:
         # budget sharding: rank r solves budget 2·M(V) − r of the sweep (all
         # budgets >= the single-segment need; per-rank work is near-identical)
@@ -384,8 +387,6 @@ def run_ours(args, world, rank, local):
         "clocks": clocks.summary(),
     }
     print(json.dumps(line), flush=True)
-    if levels:
-        comm.close()
 
 
 def main():
@@ -407,9 +408,9 @@ def main():
         run_reference(args, world, rank)
     else:
         run_ours(args, world, rank, local)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
 
+    if dist.is_available() and dist.is_initialized():
         dist.destroy_process_group()
 
 

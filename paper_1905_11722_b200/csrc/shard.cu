@@ -292,7 +292,8 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
     long long lo, hi;
     part(j0, w, c->world, c->rank, &lo, &hi);
     if ((rc = solve_level(f, lvl, lo, hi)) < 0) return rc;
-    if (c->world == 1) continue;
+    // (a one-rank communicator still runs the all-gather: the single-GPU test
+    // of the NCCL path)
     const Block bk = level_block(f, lvl, c->world);
     const size_t per = (size_t)nb * bk.bytes;
     if ((rc = c->send.ensure(per)) < 0 || (rc = c->recv.ensure(per * c->world)) < 0) return rc;

@@ -43,6 +43,24 @@ def exchange_unique_id(group=None, make=None) -> bytes:
     return box[0]
 
 
+_COMMS: dict = {}
+
+
+def communicator(device: int, group=None):
+    """This process's NCCL communicator for ``group`` on ``device``, created
+    once (ncclCommInitRank is collective and slow) and reused by every solve."""
+    dist = _dist(group)
+    key = (id(group) if group is not None else None, device, dist.get_world_size(group))
+    comm = _COMMS.get(key)
+    if comm is None or comm.handle is None:
+        from ._native import Comm
+
+        uid = exchange_unique_id(group)
+        comm = Comm(uid, dist.get_world_size(group), dist.get_rank(group), device)
+        _COMMS[key] = comm
+    return comm
+
+
 class LevelShardedSolver:
     """A (graph, family) resident on this rank's GPU, solved level-sharded."""
 
@@ -52,14 +70,12 @@ class LevelShardedSolver:
             raise ValueError(f"family must be one of {FAMILIES}, got {family!r}")
         if family == "full" and lattice_cap < g.n + 1:
             raise ValueError(f"cap must be at least n+1 = {g.n + 1}, got {lattice_cap}")
-        from ._native import Comm, DeviceFamily, DeviceGraph
+        from ._native import DeviceFamily, DeviceGraph
 
-        dist = _dist(group)
         self.graph, self.family_name = g, family
         self.dg = DeviceGraph(g, device)
         self.dev = DeviceFamily(self.dg, family, lattice_cap)
-        uid = exchange_unique_id(group)
-        self.comm = Comm(uid, dist.get_world_size(group), dist.get_rank(group), self.dg.device)
+        self.comm = communicator(self.dg.device, group)
 
     def plans(self, budgets, objective: str = "minimize"):
         if objective not in OBJECTIVES:
@@ -80,8 +96,7 @@ class LevelShardedSolver:
         return self.dev.timings()
 
     def close(self):
-        self.comm.close()
-        self.dev.close()
+        self.dev.close()  # the communicator is shared (see communicator())
         self.dg.close()
 
 

@@ -132,3 +132,44 @@ def test_wide_keys_path_matches_oracle():
         assert_plan_matches(plan, orc.dp_plan(g, 400, "full", "minimize"))
     finally:
         del os.environ["REMAT_FORCE_WIDE"]
+
+
+def _nccl_one_rank_worker(port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    from paper_1905_11722_b200 import Solver, named_graph
+    from paper_1905_11722_b200.shard import LevelShardedSolver
+
+    g = named_graph("unet", skip_len=4)
+    budgets = [2 * g.total_memory, 300]
+    ls = LevelShardedSolver(g, "full")
+    got = ls.plans(budgets)
+    ls.close()
+    s = Solver(g, "full")
+    want = s.plans(budgets)
+    s.close()
+    q.put([(a.objective_value == b.objective_value, stats_of(a) == stats_of(b),
+            a.sequence == b.sequence) for a, b in zip(got, want)])
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_level_sharded_path_one_rank():
+    """The real NCCL path (dlopen'ed libnccl, ncclCommInitRank, one
+    ncclAllGather per level on the solver's stream) on a one-rank communicator."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_one_rank_worker, args=(_free_port(), q))
+    p.start()
+    res = q.get(timeout=600)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert res == [(True, True, True)] * 2
