@@ -92,7 +92,10 @@ struct Traits<true> {
     m = v.y;
   }
   static __device__ __forceinline__ PairQN lds(const PairQN* p) {  // one LDS.128
-    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)));
     PairQN q;
     q.base = (int)v.x;
     q.cap = v.y;
@@ -408,6 +411,8 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   // so slices finish together and CTAs of a late wave find nothing left.
   // Pair constants of (predecessor i, tile target jt) -> record q; true iff
   // some frontier entry of i can pass the budget test (cap >= its smallest m).
+  // shared-window byte address of the tile rows (shared-row path)
+  const unsigned rs_base = srow ? (unsigned)__cvta_generic_to_shared(sm + ta.off_rows) : 0u;
   auto pair_q = [&](const u64 (&Li)[W], long long ii, int jt, long long MLi, long long TLi,
                     long long mmi, Q& q) {
     long long ts = 0, ms = 0;
@@ -437,7 +442,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     const long long dm = tc[jt * 4 + 3] - ms;
     const long long cap = B - fixed;
     q.cap = (MT)max(cap, 0LL);
-    q.base = 0;
+    q.base = (int)(rs_base + 4u * (unsigned)(jt * R + (int)dt));  // smem byte address of slot dt
     q.kb = (Key)(((u64)dm << IB) | (u64)ii);
     q.dtr = jt * R + (int)dt;
     return cap >= mmi;
@@ -595,18 +600,19 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         }
         if (v) {
           const Key mk = (Key)m << IB;
+          const unsigned t4 = 4u * t;
           const Q* qe = wq + rec.q1;
           const Q* qp = wq + rec.q0;
           if constexpr (NARROW) {
             if (smem) {
               for (; qp + 1 < qe; qp += 2) {
                 const Q p0 = Traits<NARROW>::lds(qp), p1 = Traits<NARROW>::lds(qp + 1);
-                relax_smem2(rs + 4u * (t + (unsigned)p0.dtr), mk + p0.kb, m <= p0.cap,
-                            rs + 4u * (t + (unsigned)p1.dtr), mk + p1.kb, m <= p1.cap);
+                relax_smem2(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap,
+                            t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
               }
               if (qp < qe) {
                 const Q p = Traits<NARROW>::lds(qp);
-                relax_smem(rs + 4u * (t + (unsigned)p.dtr), mk + p.kb, m <= p.cap);
+                relax_smem(t4 + (unsigned)p.base, mk + p.kb, m <= p.cap);
               }
               qp = qe;
             }
