@@ -52,6 +52,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxTJ = 8;    // targets per tile (one comparable bit each, <= 32)
 constexpr int kDenseLanes = 16;  // lanes with a pair for lane = predecessor constants
+constexpr int kSmallF = 4;       // frontier entries kept in registers (small-frontier path)
 
 // One relaxable (predecessor, target) pair of a warp's current group.
 struct __align__(16) PairQN {  // narrow: one LDS.128
@@ -484,6 +485,45 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       for (int w = 0; w < W; w++) Li[w] = 0;
     }
     if (!__any_sync(kFull, mask)) continue;
+    // Small frontiers (every predecessor of the chunk has <= kSmallF entries,
+    // the uniform-cost regime of deep lattices): each lane keeps its entries
+    // in registers and relaxes them into every comparable target directly —
+    // no pair records, item mapping or second pass.
+    if (__reduce_max_sync(kFull, (unsigned)fl) <= (unsigned)kSmallF) {
+      unsigned et[kSmallF];
+      MT em[kSmallF];
+#pragma unroll
+      for (int e = 0; e < kSmallF; e++) {
+        et[e] = 0;
+        em[e] = 0;
+        if (e < fl) Traits<NARROW>::load(fe + (fbase + foffi + e), et[e], em[e]);
+      }
+      for (int jt = 0; jt < ntj; jt++) {
+        const bool bit = (mask >> jt) & 1u;
+        const unsigned cm = __ballot_sync(kFull, bit);
+        const unsigned tr = __reduce_add_sync(kFull, bit ? (unsigned)fl : 0u);
+        if (lane == jt) {
+          my_pairs += __popc(cm);
+          my_trans += tr;
+        }
+        if (!bit || fl == 0) continue;
+        Q q;
+        if (!pair_q(Li, i, jt, MLi, TLi, mmi, q)) continue;
+#pragma unroll
+        for (int e = 0; e < kSmallF; e++) {
+          if (e >= fl) break;
+          const Key key = ((Key)em[e] << IB) + (Key)q.kb;
+          if constexpr (NARROW) {
+            if (srow) {
+              relax_smem((unsigned)q.base + 4u * et[e], key, em[e] <= q.cap);
+              continue;
+            }
+          }
+          if (em[e] <= q.cap) key_min(rows + (et[e] + q.dtr), key, srow);
+        }
+      }
+      continue;
+    }
     // per target: statistics, then the pair constants — computed right here
     // (lane = predecessor, no reload) when most lanes hold a pair, else
     // deferred to a compacted list (lane = pair) so sparse targets do not
