@@ -728,6 +728,20 @@ __global__ void __launch_bounds__(kThreads)
   relax_body<W, NARROW>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
 }
 
+// wide bitsets (W >= 4) keep three CTAs per SM resident (<= 80 registers)
+template <int W, bool NARROW>
+__global__ void __launch_bounds__(kThreads, 3)
+    k_relax_tile3(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  relax_body<W, NARROW>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
+}
+
+template <int W, bool NARROW>
+static constexpr auto relax_tile_kernel() {
+  if constexpr (W >= 4) return k_relax_tile3<W, NARROW>;
+  else return k_relax_tile<W, NARROW>;
+}
+
 // Several consecutive small levels in ONE cooperative launch: every block
 // walks the (tile, split, budget) virtual CTAs of a level, then a grid barrier
 // publishes the level (its tiles were finalized by their last CTA) before the
@@ -930,7 +944,7 @@ static int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int
     return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    RM_CUDA(cudaFuncSetAttribute(k_relax_tile<W, NARROW>,
+    RM_CUDA(cudaFuncSetAttribute(relax_tile_kernel<W, NARROW>(),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
     attr_set = true;
   }
@@ -1036,8 +1050,8 @@ static int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   if (hi <= lo) return REMAT_OK;
   int rc = plan_level_w<W, NARROW>(f, lvl, lo, hi, ta);
   if (rc < 0) return rc;
-  k_relax_tile<W, NARROW><<<dim3((unsigned)(ta.tiles * ta.splits), (unsigned)f->cur_nb), kThreads,
-                            ta.bytes, f->g->stream>>>(f->view(), f->g->view(), f->g->classes(),
+  relax_tile_kernel<W, NARROW>()<<<dim3((unsigned)(ta.tiles * ta.splits), (unsigned)f->cur_nb),
+                                   kThreads, ta.bytes, f->g->stream>>>(f->view(), f->g->view(), f->g->classes(),
                                                       f->dp_view(), ta);
   RM_LAUNCHED();
   f->relax_launches++;
