@@ -509,7 +509,9 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
     // (b) partial ranks of level k over (element tile, comparison tile) tasks
     if (k <= n) {
       const long long nt = (N + 255) / 256;
-      for (long long task = blockIdx.x; task < nt * nt; task += gridDim.x) {
+      // (from the last block down: when the level is narrow the first blocks
+      // carry the emission tasks, so ranking runs beside them, not after)
+      for (long long task = gridDim.x - 1 - blockIdx.x; task < nt * nt; task += gridDim.x) {
         const long long it = task / nt, tt = task - it * nt;
         const long long i = it * 256 + threadIdx.x, t0 = tt * 256;
         const long long c = min(256LL, N - t0);
