@@ -3,7 +3,7 @@ timeout 600 python - <<'PY'
 import sys, time
 sys.path.insert(0,'.')
 from paper_1905_11722_b200 import named_graph, Solver
-for p in (0.25, 0.2):
+for p in (0.4, 0.3, 0.25, 0.2):
     g=named_graph('random-dag',depth=516,edge_prob=p,seed=0)
     t=time.time(); s=Solver(g,'full'); t1=time.time()
     pl=s.plan(2*g.total_memory); t2=time.time()
