@@ -87,8 +87,10 @@ struct Traits<true> {
   static constexpr unsigned INF = 0xffffffffu;
   // one LDG.64 per entry (entries of earlier levels are read-only while a
   // level is relaxed, so the non-coherent path is safe)
+  template <bool COH = false>
   static __device__ __forceinline__ void load(const E* p, unsigned& t, unsigned& m) {
-    const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+    const uint2* q = reinterpret_cast<const uint2*>(p);
+    const uint2 v = COH ? __ldcg(q) : __ldg(q);
     t = v.x;
     m = v.y;
   }
@@ -112,8 +114,10 @@ struct Traits<false> {
   using Q = PairQW;
   using M = long long;
   static constexpr u64 INF = ~0ull;
+  template <bool COH = false>
   static __device__ __forceinline__ void load(const E* p, unsigned& t, long long& m) {
-    const longlong2 v = __ldg(reinterpret_cast<const longlong2*>(p));
+    const longlong2* q = reinterpret_cast<const longlong2*>(p);
+    const longlong2 v = COH ? __ldcg(q) : __ldg(q);
     t = (unsigned)v.x;
     m = v.y;
   }
@@ -326,7 +330,10 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
 // K4 (+K5): one (tile, split) "virtual CTA" `vbx` of budget b.  Run either as
 // one CTA of k_relax_tile (grid (tiles·splits, nb)) or inside the persistent
 // k_relax_levels loop.
-template <int W, bool NARROW>
+// COH: the table being read was written earlier in the SAME launch (persistent
+// multi-level kernel) — frontier entries and per-member records are then read
+// through L2 (ld.cg), never the non-coherent path.
+template <int W, bool NARROW, bool COH>
 __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView& g,
                                            const ClassView& cv, const DpView& dp,
                                            const TileArgs& ta, const int vbx, const int b,
@@ -469,8 +476,8 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     if (i < pred_end) {
 #pragma unroll
       for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + i);
-      fl = flen_b[i];
-      mmi = mmin_b[i];
+      fl = COH ? __ldcg(flen_b + i) : flen_b[i];
+      mmi = COH ? __ldcg(mmin_b + i) : mmin_b[i];
       MLi = __ldg(fv.ML + i);
       TLi = __ldg(fv.TL + i);
       foffi = __ldg(fv.foff + i);
@@ -496,7 +503,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       for (int e = 0; e < kSmallF; e++) {
         et[e] = 0;
         em[e] = 0;
-        if (e < fl) Traits<NARROW>::load(fe + (fbase + foffi + e), et[e], em[e]);
+        if (e < fl) Traits<NARROW>::template load<COH>(fe + (fbase + foffi + e), et[e], em[e]);
       }
       for (int jt = 0; jt < ntj; jt++) {
         const bool bit = (mask >> jt) & 1u;
@@ -573,7 +580,8 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
 #pragma unroll
         for (int w = 0; w < W; w++) Lp[w] = __ldg(fv.masks + (size_t)w * F + ii);
         Q q;
-        if (pair_q(Lp, ii, jt, __ldg(fv.ML + ii), __ldg(fv.TL + ii), mmin_b[ii], q))
+        if (pair_q(Lp, ii, jt, __ldg(fv.ML + ii), __ldg(fv.TL + ii),
+                   COH ? __ldcg(mmin_b + ii) : mmin_b[ii], q))
           wq[pl * TJ + atomicAdd(wpc + pl, 1)] = q;
       }
     }
@@ -622,7 +630,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         v = lane < tot;
         if (v) {
           rec = wrec[k];
-          Traits<NARROW>::load(fe + (rec.base + lane), t, m);
+          Traits<NARROW>::template load<COH>(fe + (rec.base + lane), t, m);
         }
       }
       for (int r = 0; r < tot; r += 32) {
@@ -635,7 +643,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           vn = r + 32 + lane < tot;
           if (vn) {
             recn = wrec[kn];
-            Traits<NARROW>::load(fe + (recn.base + r + 32 + lane), tn, mn);
+            Traits<NARROW>::template load<COH>(fe + (recn.base + r + 32 + lane), tn, mn);
           }
         }
         if (v) {
@@ -725,7 +733,7 @@ template <int W, bool NARROW>
 __global__ void __launch_bounds__(kThreads)
     k_relax_tile(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
   extern __shared__ __align__(16) unsigned char sm[];
-  relax_body<W, NARROW>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
+  relax_body<W, NARROW, false>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
 }
 
 // wide bitsets (W >= 4) keep three CTAs per SM resident (<= 80 registers)
@@ -733,13 +741,36 @@ template <int W, bool NARROW>
 __global__ void __launch_bounds__(kThreads, 3)
     k_relax_tile3(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
   extern __shared__ __align__(16) unsigned char sm[];
-  relax_body<W, NARROW>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
+  relax_body<W, NARROW, false>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
 }
 
 template <int W, bool NARROW>
 static constexpr auto relax_tile_kernel() {
   if constexpr (W >= 4) return k_relax_tile3<W, NARROW>;
   else return k_relax_tile<W, NARROW>;
+}
+
+// A whole small family in ONE launch: one CTA per budget walks every level's
+// tiles itself (rows in shared memory, no splits), with only CTA barriers
+// between levels — for pruned families and chain-like lattices whose hundreds
+// of levels are each far too small for the GPU (C1, C3).
+template <int W, bool NARROW>
+__global__ void __launch_bounds__(kThreads)
+    k_solve_small(FamilyView fv, GraphView g, ClassView cv, DpView dp,
+                  const TileArgs* __restrict__ levels, int nlev, int nb) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int b = blockIdx.y;
+  for (int l = 0; l < nlev; l++) {
+    const TileArgs ta = levels[l];
+    for (int t = 0; t < ta.tiles; t++) {
+      relax_body<W, NARROW, true>(fv, g, cv, dp, ta, t, b, nb, sm);
+      __syncthreads();
+    }
+    // the next level reads this one through L2 (ld.cg): make the finalized
+    // frontier entries and records visible there before any warp proceeds
+    __threadfence();
+    __syncthreads();
+  }
 }
 
 // Several consecutive small levels in ONE cooperative launch: every block
@@ -758,7 +789,7 @@ __global__ void __launch_bounds__(kThreads)
     const TileArgs ta = levels[l];
     const int per = ta.tiles * ta.splits;
     for (int v = blockIdx.x; v < per * nb; v += gridDim.x) {
-      relax_body<W, NARROW>(fv, g, cv, dp, ta, v % per, v / per, nb, sm);
+      relax_body<W, NARROW, true>(fv, g, cv, dp, ta, v % per, v / per, nb, sm);
       __syncthreads();
     }
     grid.sync();
@@ -915,6 +946,8 @@ static constexpr int kRowBudget = 64 * 1024;   // tile rows per CTA (4 CTAs/SM)
 // into one cooperative launch (their work is a fraction of one GPU wave)
 static constexpr long long kSmallLevelTests = 4LL << 20;
 static constexpr long long kSmallLevelPreds = 32LL << 10;
+// families up to this size are solved by one CTA per budget (k_solve_small)
+static constexpr long long kSmallFamily = 1100;
 
 // The solve in three phases so the level loop can be driven from outside
 // (level sharding, shard.cu): begin (buffers + the empty set), one call per
@@ -992,7 +1025,7 @@ static int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int
 
 template <int W, bool NARROW>
 static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArgs& ta,
-                        long long max_vctas = 0) {
+                        long long max_vctas = 0, bool single_cta = false) {
   using Key = typename Traits<NARROW>::Key;
   remat_graph_s* g = f->g;
   cudaStream_t s = g->stream;
@@ -1016,7 +1049,7 @@ static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, 
   // fewer targets per tile where the level is too small to give every
   // resident warp a couple of (tile, chunk) tasks
   const long long want = (long long)num_sms * 64;
-  while (TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
+  while (!single_cta && TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
   const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
   ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
   if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
@@ -1025,6 +1058,7 @@ static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, 
   // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
   long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
   if (max_vctas > 0) splits = max_vctas / (tiles * nb);  // persistent: one round per block
+  if (single_cta) splits = 1;
   splits = std::max(1LL, std::min(splits, nch / kWarps));
   ta.jbase = lo;
   ta.pend = j0;
@@ -1115,6 +1149,40 @@ static int levels_w(remat_family_s* f, const std::vector<int>& lvls) {
   RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_relax_levels<W, NARROW>,
                                       dim3((unsigned)(num_sms * std::min(bps, 4))), dim3(kThreads),
                                       args, (size_t)maxbytes, s));
+  RM_LAUNCHED();
+  f->relax_launches++;
+  return REMAT_OK;
+}
+
+// The whole family in one k_solve_small launch (one CTA per budget).  Returns
+// 1 without launching when some level's rows do not fit shared memory.
+template <int W, bool NARROW>
+static int small_w(remat_family_s* f) {
+  const int n = f->g->n;
+  std::vector<TileArgs> tas;
+  int maxbytes = 0, rc;
+  for (int l = 1; l <= n; l++) {
+    const long long j0 = f->level_start[l], j1 = f->level_start[l + 1];
+    if (j1 == j0) continue;
+    TileArgs ta;
+    if ((rc = plan_level_w<W, NARROW>(f, l, j0, j1, ta, 0, true)) < 0) return rc;
+    if (!ta.smem_rows) return 1;
+    maxbytes = std::max(maxbytes, ta.bytes);
+    tas.push_back(ta);
+  }
+  static bool attr = false;
+  if (!attr) {
+    RM_CUDA(cudaFuncSetAttribute(k_solve_small<W, NARROW>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    attr = true;
+  }
+  cudaStream_t s = f->g->stream;
+  if ((rc = f->levelargs.ensure(tas.size() * sizeof(TileArgs))) < 0) return rc;
+  RM_CUDA(cudaMemcpyAsync(f->levelargs.p, tas.data(), tas.size() * sizeof(TileArgs),
+                          cudaMemcpyHostToDevice, s));
+  k_solve_small<W, NARROW><<<dim3(1, (unsigned)f->cur_nb), kThreads, (size_t)maxbytes, s>>>(
+      f->view(), f->g->view(), f->g->classes(), f->dp_view(),
+      reinterpret_cast<const TileArgs*>(f->levelargs.p), (int)tas.size(), f->cur_nb);
   RM_LAUNCHED();
   f->relax_launches++;
   return REMAT_OK;
@@ -1238,6 +1306,12 @@ int solve_levels(remat_family_s* f, const std::vector<int>& lvls) {
   });
 }
 
+int solve_small(remat_family_s* f) {
+  return dispatch_solve(f, f->cur_narrow, [&](auto wc, auto nc) {
+    return small_w<decltype(wc)::value, decltype(nc)::value>(f);
+  });
+}
+
 int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                  long long* stage_memory) {
   return dispatch_solve(f, f->cur_narrow, [&](auto wc, auto nc) {
@@ -1251,6 +1325,12 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
                 long long* stage_memory) {
   int rc = solve_begin(f, budgets, objective);
   if (rc < 0) return rc;
+  // a small family (pruned families, chain-like lattices) runs whole in one
+  // CTA per budget
+  if (f->F <= kSmallFamily) {
+    if ((rc = solve_small(f)) < 0) return rc;
+    if (rc == REMAT_OK) return solve_finish(f, info, chain_masks, cached_masks, stage_memory);
+  }
   // levels whose subset tests fit one wave of the GPU run back to back in a
   // single cooperative launch; wide levels get their own launch
   std::vector<int> run;

@@ -27,6 +27,7 @@ FAMILIES = ("full", "pruned")
 OBJECTIVES = ("minimize", "maximize")
 
 DEFAULT_DFS_STATE_CAP = 10_000_000
+SMALL_FAMILY = 1100  # csrc/relax.cu kSmallFamily: one CTA per budget
 
 
 class PlannerError(RuntimeError):
@@ -128,9 +129,13 @@ class Solver:
         return self.plans([budget], objective)[0]
 
     def min_feasible_budget(self, objective: str = "minimize",
-                            probes_per_round: int = 8) -> tuple[int, PlanResult]:
+                            probes_per_round: int | None = None) -> tuple[int, PlanResult]:
         if objective not in OBJECTIVES:
             raise ValueError(f"objective must be one of {OBJECTIVES}, got {objective!r}")
+        if probes_per_round is None:
+            # small families solve one budget per CTA: a round of 48 probes costs
+            # what one probe does, so the search takes few, wide rounds
+            probes_per_round = 48 if self.dev.size <= SMALL_FAMILY else 8
         t0 = time.perf_counter()
         bmin, raw, search = self.dev.min_feasible_budget(objective, probes_per_round)
         wall = time.perf_counter() - t0
