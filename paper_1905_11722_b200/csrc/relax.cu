@@ -136,8 +136,10 @@ struct TileArgs {
   int cls;          // weight-class path available
   int rows_pb;      // rows per budget in grow (tiles · TJ)
   void* grow;       // [nb][rows_pb][R] global rows (split / oversized levels)
-  unsigned* ctr;    // [nb][tiles] next predecessor chunk of the tile (zeroed per level)
+  unsigned* ctr;    // [nb][ctr_stride] next predecessor chunk of the tile (left zero)
   int tiles;
+  int ctr_stride;   // counters per budget: tiles, or the widest level when budgets run
+                    // through the levels independently (k_solve_small)
   int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_coef, off_tacc, off_pairs, off_q, off_qs, off_rows;
   int bytes;
 };
@@ -410,7 +412,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   const E* fe = reinterpret_cast<const E*>(dp.fe);
   const long long pred_end = ta.pend;
   const long long nch = (pred_end + 31) / 32;
-  unsigned* ctr = ta.ctr + (size_t)b * ta.tiles + tile;
+  unsigned* ctr = ta.ctr + (size_t)b * ta.ctr_stride + tile;
   u64 my_trans = 0;  // lane jt accumulates target jt of the tile
   u64 my_pairs = 0;
   bool worked = false;
@@ -695,7 +697,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     if (tacc[tid * 2 + 1])
       atomicAdd(reinterpret_cast<unsigned long long*>(dp.npairs + at), tacc[tid * 2 + 1]);
   }
-  unsigned* done = ctr + (size_t)nb * ta.tiles;  // finished CTAs of the tile
+  unsigned* done = ctr + (size_t)nb * ta.ctr_stride;  // finished CTAs of the tile
   if (splits == 1 && srow) {
     for (int jt = warp; jt < ntj; jt += kWarps)
       finalize_row_warp<NARROW>(rows + jt * R, (int)(fv.TL[j0 + jt] + 1), dp,
@@ -1067,6 +1069,7 @@ static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, 
   ta.grow = nullptr;
   ta.rows_pb = (int)(tiles * TJ);
   ta.tiles = (int)tiles;
+  ta.ctr_stride = (int)tiles;
   ta.ctr = f->ctr.p;  // [nb][tiles] chunk counters + [nb][tiles] done counters, all zero
   if ((size_t)2 * nb * tiles > f->ctr_cap)
     return fail(REMAT_ERR_INTERNAL, "tile counter capacity exceeded");
@@ -1170,6 +1173,10 @@ static int small_w(remat_family_s* f) {
     maxbytes = std::max(maxbytes, ta.bytes);
     tas.push_back(ta);
   }
+  // budgets walk the levels independently: give each budget its own counters
+  int stride = 1;
+  for (auto& ta : tas) stride = std::max(stride, ta.tiles);
+  for (auto& ta : tas) ta.ctr_stride = stride;
   static bool attr = false;
   if (!attr) {
     RM_CUDA(cudaFuncSetAttribute(k_solve_small<W, NARROW>,
