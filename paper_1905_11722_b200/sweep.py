@@ -71,3 +71,60 @@ def budget_sweep(g, budgets: Sequence[int], family: str = "pruned",
     gathered: list = [None] * world
     dist.all_gather_object(gathered, local, group=group)
     return [p for part in gathered for p in part]
+
+
+def min_feasible_budget_sharded(g, family: str = "full", objective: str = "minimize",
+                                lattice_cap: int = DEFAULT_LATTICE_CAP, probes_per_rank: int = 8,
+                                solve: Callable | None = None, group=None):
+    """``min_feasible_budget`` (reference planner.py:271-297) with the probes of
+    every search round spread over the ranks (one probe batch per
+    GPU per round).  Feasibility is monotone in the budget, so
+    any probe order finds the reference's B_min; the returned plan is the
+    solve at B_min.  Each rank keeps one family resident for the whole search;
+    a round exchanges only (budget, feasible) pairs.
+
+    ``solve(g, budgets, family, objective, cap) -> list of plans`` with a
+    ``feasible`` attribute or key (default: this rank's GPU ``Solver``)."""
+    dist = _dist()
+    world = dist.get_world_size(group) if dist else 1
+    rank = dist.get_rank(group) if dist else 0
+    solver = None
+    if solve is None:
+        from .planner import Solver
+
+        solver = Solver(g, family, lattice_cap)
+
+        def solve(g, bs, family, objective, cap):
+            return solver.plans(bs, objective) if bs else []
+
+    def feasible(p):
+        return p["feasible"] if isinstance(p, dict) else p.feasible
+
+    try:
+        hi = 2 * g.total_memory            # always feasible (SURVEY App. A.5)
+        lo = 2 * max(g.memory_costs) - 1   # no stage fits below 2·max_v M_v
+        best = None                        # (budget, plan) of the smallest feasible probe
+        while hi - lo > 1:
+            k = world * probes_per_rank
+            probes = sorted({lo + (hi - lo) * q // (k + 1) for q in range(1, k + 1)} - {lo, hi})
+            if not probes:
+                probes = [lo + (hi - lo) // 2]
+            mine = shard(probes, world, rank)
+            got = list(zip(mine, (feasible(p) for p in solve(g, mine, family, objective,
+                                                              lattice_cap))))
+            if world > 1:
+                parts: list = [None] * world
+                dist.all_gather_object(parts, got, group=group)
+                got = [x for part in parts for x in part]
+            ok = [b for b, f in got if f]
+            if ok:
+                hi = min(ok)
+                below = [b for b, _ in got if b < hi]
+                lo = max(below) if below else lo
+            else:
+                lo = max(b for b, _ in got)
+        plan = solve(g, [hi], family, objective, lattice_cap)[0]
+        return hi, plan
+    finally:
+        if solver is not None:
+            solver.close()
