@@ -4,5 +4,5 @@
 mkdir -p gpurun_out
 W=${1:-unet}; shift
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-  -k regex:k_relax_tile --csv --log-file gpurun_out/traffic_$W.csv python tools/solve_once.py --workload $W "$@" > /dev/null 2>&1
+  -k regex:k_relax --csv --log-file gpurun_out/traffic_$W.csv python tools/solve_once.py --workload $W "$@" > /dev/null 2>&1
 echo traffic done
