@@ -335,7 +335,7 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
 // COH: the table being read was written earlier in the SAME launch (persistent
 // multi-level kernel) — frontier entries and per-member records are then read
 // through L2 (ld.cg), never the non-coherent path.
-template <int W, bool NARROW, bool COH>
+template <int W, bool NARROW, bool COH, bool DUAL = false>
 __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView& g,
                                            const ClassView& cv, const DpView& dp,
                                            const TileArgs& ta, const int vbx, const int b,
@@ -678,11 +678,98 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         v = vn;
       }
     };
-    if (srow)
-      relax_items(reinterpret_cast<Key*>(sm + ta.off_rows),
-                  (unsigned)__cvta_generic_to_shared(sm + ta.off_rows), true);
-    else
-      relax_items(grow_t, 0u, false);
+    auto relax_items2 = [&](Key* __restrict__ rw, const unsigned rs, const bool smem) {
+      int kbase = -1;
+      // 64 items per step, lane owns items 2·lane and 2·lane+1 of the step:
+      // two REDUX.OR gather the predecessor starts in each half, popcounts
+      // rank both items (warp-uniform call)
+      auto map_step = [&](int r, int& k0, int& k1) {
+        const unsigned d = (unsigned)(start - r);
+        const unsigned lo = __reduce_or_sync(kFull, d < 32u ? 1u << d : 0u);
+        const unsigned hi = __reduce_or_sync(kFull, d - 32u < 32u ? 1u << (d - 32u) : 0u);
+        const unsigned m0 = (2u << ((2 * lane) & 31)) - 1, m1 = (2u << ((2 * lane + 1) & 31)) - 1;
+        const int below = lane < 16 ? 0 : __popc(lo);
+        const unsigned half = lane < 16 ? lo : hi;
+        k0 = kbase + below + __popc(half & m0);
+        k1 = kbase + below + __popc(half & m1);
+        kbase += __popc(lo) + __popc(hi);
+      };
+      struct Item {
+        PredRec rec;
+        unsigned t;
+        MT m;
+        bool v;
+      };
+      auto fetch = [&](int r, Item& x0, Item& x1) {
+        int k0, k1;
+        map_step(r, k0, k1);
+        const int e0 = r + 2 * lane;
+        x0.v = e0 < tot;
+        x1.v = e0 + 1 < tot;
+        if (x0.v) {
+          x0.rec = wrec[k0];
+          Traits<NARROW>::template load<COH>(fe + (x0.rec.base + e0), x0.t, x0.m);
+        }
+        if (x1.v) {
+          x1.rec = wrec[k1];
+          Traits<NARROW>::template load<COH>(fe + (x1.rec.base + e0 + 1), x1.t, x1.m);
+        }
+      };
+      auto relax = [&](const Item& x) {
+        const unsigned t = x.t;
+        const MT m = x.m;
+        const Key mk = (Key)m << IB;
+        const unsigned t4 = 4u * t;
+        const Q* qe = wq + x.rec.q1;
+        const Q* qp = wq + x.rec.q0;
+        if constexpr (NARROW) {
+          if (smem) {
+            for (; qp + 1 < qe; qp += 2) {
+              const Q p0 = Traits<NARROW>::lds(qp), p1 = Traits<NARROW>::lds(qp + 1);
+              relax_smem2(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap,
+                          t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
+            }
+            if (qp < qe) {
+              const Q p = Traits<NARROW>::lds(qp);
+              relax_smem(t4 + (unsigned)p.base, mk + p.kb, m <= p.cap);
+            }
+            return;
+          }
+        }
+        for (; qp < qe; ++qp) {
+          const Q p = Traits<NARROW>::lds(qp);
+          if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
+        }
+      };
+      // software-pipelined: the two entries of step r+64 are in flight (L2)
+      // while the targets of step r are relaxed
+      Item a0{}, a1{};
+      fetch(0, a0, a1);
+      for (int r = 0; r < tot; r += 64) {
+        Item b0{}, b1{};
+        if (r + 64 < tot) fetch(r + 64, b0, b1);
+        if (a0.v) relax(a0);
+        if (a1.v) relax(a1);
+        a0 = b0;
+        a1 = b1;
+      }
+    };
+    // throughput launches relax 32 items per warp step; the one-CTA-per-budget
+    // solver (few warps per level, L2-latency bound) takes 64 with two loads
+    // in flight per lane
+    if constexpr (DUAL) {
+      if (srow)
+        relax_items2(reinterpret_cast<Key*>(sm + ta.off_rows),
+                     (unsigned)__cvta_generic_to_shared(sm + ta.off_rows), true);
+      else
+        relax_items2(grow_t, 0u, false);
+    } else {
+      if (srow)
+        relax_items(reinterpret_cast<Key*>(sm + ta.off_rows),
+                    (unsigned)__cvta_generic_to_shared(sm + ta.off_rows), true);
+      else
+        relax_items(grow_t, 0u, false);
+    }
     __syncwarp();
   }
   if (lane == 0 && worked) s_worked = 1;
@@ -765,7 +852,7 @@ __global__ void __launch_bounds__(kThreads)
   for (int l = 0; l < nlev; l++) {
     const TileArgs ta = levels[l];
     for (int t = 0; t < ta.tiles; t++) {
-      relax_body<W, NARROW, true>(fv, g, cv, dp, ta, t, b, nb, sm);
+      relax_body<W, NARROW, true, true>(fv, g, cv, dp, ta, t, b, nb, sm);
       __syncthreads();
     }
     // the next level reads this one through L2 (ld.cg): make the finalized
