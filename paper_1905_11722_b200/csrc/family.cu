@@ -439,10 +439,12 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 // Buffers rotate over three slots, so each is written one step after its
 // last reader finished.
 //   ctr[k]    |level k| (ctr[0] = 1: the empty set, pre-set by the host)
-//   status[0] 1 when the lattice exceeds `cap` (LatticeTooLargeError)
+//   status[0] 1 when the lattice exceeds `cap` (LatticeTooLargeError), 2 when
+//             it exceeds the buffers' capacity `fcap` (< cap): grow and rerun
 template <int W>
 __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds, int n,
-                                                  long long cap, u64* __restrict__ fam,
+                                                  long long cap, long long fcap,
+                                                  u64* __restrict__ fam,
                                                   u64* __restrict__ U, long long ucap,
                                                   unsigned* __restrict__ rank,
                                                   long long* __restrict__ ctr,
@@ -460,8 +462,8 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
   long long base = 0, prev_base = 0, prevN = 0;  // ls[k], ls[k-1], |level k-1|
   for (int k = 0; k <= n + 1; k++) {
     const long long N = k <= n ? *((volatile long long*)(ctr + k)) : 0;
-    if (base + N > cap) {  // uniform: every block read the same counters
-      if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = 1;
+    if (base + N > cap || base + N > fcap) {  // uniform: every block read the same counters
+      if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = base + N > cap ? 1 : 2;
       return;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && k <= n) ls[k] = base;
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
     const u64* prv = U + (size_t)((k + 2) % 3) * ucap * 2 * W;
     unsigned* rk = rank + (size_t)(k % 3) * ucap;
     unsigned* rkp = rank + (size_t)((k + 2) % 3) * ucap;
-    const long long room = min(cap - base - N, ucap);  // children that fit
+    const long long room = min(min(cap, fcap) - base - N, ucap);  // children that fit
     // (c) scatter level k-1, leaving its rank slot zeroed for level k+2
     for (long long i = gt; i < prevN; i += nthreads) {
       const long long at = prev_base + rkp[i];
@@ -544,13 +546,15 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
                           std::vector<long long>& level_start) {
   cudaStream_t s = g->stream;
   const int n = g->n;
-  // the family is sized for the cap (a larger lattice raises
-  // LatticeTooLargeError); the three level buffers hold one level each, and
-  // no level is wider than C(n, n/2) nor than the cap
-  const long long Fcap = std::max<long long>(cap, n + 1);
+  // Buffers start at min(cap, 4 M members) and grow 4x (rerun) only when the
+  // lattice outgrows them below the cap; the three level buffers hold one
+  // level each, and no level is wider than C(n, n/2) nor than the family.
+  const long long capn = std::max<long long>(cap, n + 1);
+  long long fcap = std::min<long long>(capn, 4LL << 20);
+  if (const char* e = getenv("REMAT_ENUM_INIT_CAP"))  // test hook for the grow path
+    fcap = std::min<long long>(capn, std::max<long long>(n + 1, atoll(e)));
   long double binom = 1;
   for (int i = 1; i <= n / 2; i++) binom = binom * (n - n / 2 + i) / i;
-  const long long ucap = (long long)std::min<long double>((long double)Fcap, binom + 1);
   int rc;
   DevBuf<u64> U;
   DevBuf<unsigned> rank;
@@ -563,38 +567,43 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
   if (bps < 1) return fail(REMAT_ERR_CUDA, "enumeration kernel cannot be resident");
   // one block per SM keeps the per-level grid barrier cheap
   const int nblk = num_sms;
-  if ((rc = fam.ensure((size_t)Fcap * W)) < 0 || (rc = U.ensure((size_t)3 * ucap * 2 * W)) < 0 ||
-      (rc = rank.ensure((size_t)3 * ucap)) < 0 || (rc = ctr.ensure(n + 2)) < 0 ||
-      (rc = ls.ensure(n + 2)) < 0 || (rc = status.ensure(1)) < 0)
+  if ((rc = ctr.ensure(n + 2)) < 0 || (rc = ls.ensure(n + 2)) < 0 || (rc = status.ensure(1)) < 0)
     return rc;
-  RM_CUDA(cudaMemsetAsync(U.p, 0, sizeof(u64) * 2 * W, s));  // the empty set, no maximal elements
-  RM_CUDA(cudaMemsetAsync(rank.p, 0, sizeof(unsigned) * 3 * ucap, s));
-  RM_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(long long) * (n + 2), s));
-  RM_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
-  const long long one = 1;
-  RM_CUDA(cudaMemcpyAsync(ctr.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
-  const u64* preds = g->preds.p;
-  u64 *a0 = fam.p, *a1 = U.p;
-  long long uc = ucap;
-  unsigned* a2 = rank.p;
-  long long *a3 = ctr.p, *a4 = ls.p;
-  int* a5 = status.p;
-  int nn = n;
-  long long cp = cap;
-  void* args[] = {(void*)&preds, &nn, &cp, &a0, &a1, &uc, &a2, &a3, &a4, &a5};
-  RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_enum_all<W>, dim3(nblk), dim3(256), args, 0,
-                                      s));
-  RM_LAUNCHED();
-  int st = 0;
-  level_start.assign(n + 2, 0);
-  RM_CUDA(cudaMemcpyAsync(&st, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-  RM_CUDA(cudaMemcpyAsync(level_start.data(), ls.p, sizeof(long long) * (n + 2),
-                          cudaMemcpyDeviceToHost, s));
-  RM_CUDA(cudaStreamSynchronize(s));
-  if (st)
-    return fail(REMAT_ERR_LATTICE, "lattice too large: more than " + std::to_string(cap) +
-                                       " lower sets; raise the cap or use the pruned family");
-  return REMAT_OK;
+  while (true) {
+    const long long ucap = (long long)std::min<long double>((long double)fcap, binom + 1);
+    if ((rc = fam.ensure((size_t)fcap * W)) < 0 || (rc = U.ensure((size_t)3 * ucap * 2 * W)) < 0 ||
+        (rc = rank.ensure((size_t)3 * ucap)) < 0)
+      return rc;
+    RM_CUDA(cudaMemsetAsync(U.p, 0, sizeof(u64) * 2 * W, s));  // the empty set, no maximal elements
+    RM_CUDA(cudaMemsetAsync(rank.p, 0, sizeof(unsigned) * 3 * ucap, s));
+    RM_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(long long) * (n + 2), s));
+    RM_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+    const long long one = 1;
+    RM_CUDA(cudaMemcpyAsync(ctr.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
+    const u64* preds = g->preds.p;
+    u64 *a0 = fam.p, *a1 = U.p;
+    long long uc = ucap, fc = fcap;
+    unsigned* a2 = rank.p;
+    long long *a3 = ctr.p, *a4 = ls.p;
+    int* a5 = status.p;
+    int nn = n;
+    long long cp = cap;
+    void* args[] = {(void*)&preds, &nn, &cp, &fc, &a0, &a1, &uc, &a2, &a3, &a4, &a5};
+    RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_enum_all<W>, dim3(nblk), dim3(256), args,
+                                        0, s));
+    RM_LAUNCHED();
+    int st = 0;
+    level_start.assign(n + 2, 0);
+    RM_CUDA(cudaMemcpyAsync(&st, status.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaMemcpyAsync(level_start.data(), ls.p, sizeof(long long) * (n + 2),
+                            cudaMemcpyDeviceToHost, s));
+    RM_CUDA(cudaStreamSynchronize(s));
+    if (st == 1)
+      return fail(REMAT_ERR_LATTICE, "lattice too large: more than " + std::to_string(cap) +
+                                         " lower sets; raise the cap or use the pruned family");
+    if (st == 0) return REMAT_OK;
+    fcap = std::min<long long>(capn, fcap * 4);  // outgrew the buffers: grow and rerun
+  }
 }
 
 template <int W>
