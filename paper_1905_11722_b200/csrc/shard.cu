@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -286,14 +287,17 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
   int rc;
   if ((rc = ensure_foff(f)) < 0 || (rc = solve_begin(f, bs, objective)) < 0) return rc;
   SegList sl;
+  const char* fx = getenv("REMAT_SHARD_EXCHANGE");
+  const bool force_exchange = fx && fx[0] == '1';
   for (int lvl = 1; lvl <= g->n; lvl++) {
     const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
     if (w == 0) continue;
     long long lo, hi;
     part(j0, w, c->world, c->rank, &lo, &hi);
     if ((rc = solve_level(f, lvl, lo, hi)) < 0) return rc;
-    // (a one-rank communicator still runs the all-gather: the single-GPU test
-    // of the NCCL path)
+    // a one-rank communicator has nothing to exchange (REMAT_SHARD_EXCHANGE=1
+    // still runs the all-gather: the single-GPU test of the NCCL path)
+    if (c->world == 1 && !force_exchange) continue;
     const Block bk = level_block(f, lvl, c->world);
     const size_t per = (size_t)nb * bk.bytes;
     if ((rc = c->send.ensure(per)) < 0 || (rc = c->recv.ensure(per * c->world)) < 0) return rc;

@@ -144,6 +144,7 @@ def _nccl_one_rank_worker(port, q):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["REMAT_SHARD_EXCHANGE"] = "1"  # run the all-gather even on one rank
     dist.init_process_group("gloo", rank=0, world_size=1)
     from paper_1905_11722_b200 import Solver, named_graph
     from paper_1905_11722_b200.shard import LevelShardedSolver
