@@ -138,6 +138,7 @@ struct TileArgs {
   void* grow;       // [nb][rows_pb][R] global rows (split / oversized levels)
   unsigned* ctr;    // [nb][ctr_stride] next predecessor chunk of the tile (left zero)
   int tiles;
+  int cw;           // predecessors per chunk (<= 32)
   int ctr_stride;   // counters per budget: tiles, or the widest level when budgets run
                     // through the levels independently (k_solve_small)
   int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_coef, off_tacc, off_pairs, off_q, off_qs, off_rows;
@@ -411,7 +412,8 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   const long long* mmin_b = dp.mmin + (size_t)b * F;
   const E* fe = reinterpret_cast<const E*>(dp.fe);
   const long long pred_end = ta.pend;
-  const long long nch = (pred_end + 31) / 32;
+  const int cw = ta.cw;  // predecessors per chunk (32; fewer spreads narrow levels over warps)
+  const long long nch = (pred_end + cw - 1) / cw;
   unsigned* ctr = ta.ctr + (size_t)b * ta.ctr_stride + tile;
   u64 my_trans = 0;  // lane jt accumulates target jt of the tile
   u64 my_pairs = 0;
@@ -470,12 +472,12 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
        ch = next_chunk()) {
     worked = true;
     // lane = predecessor i: its set and scalars in one round of loads
-    const long long i = ch * 32 + lane;
+    const long long i = ch * cw + lane;
     u64 Li[W];
     int fl = 0;
     long long MLi = 0, TLi = 0, mmi = 0, foffi = 0;
     unsigned mask = 0;
-    if (i < pred_end) {
+    if (lane < cw && i < pred_end) {
 #pragma unroll
       for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + i);
       fl = COH ? __ldcg(flen_b + i) : flen_b[i];
@@ -577,7 +579,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       if (lane < nsp - g0) {
         const int pr = wpairs[g0 + lane];
         const int jt = pr & 31, pl = pr >> 5;
-        const long long ii = ch * 32 + pl;
+        const long long ii = ch * cw + pl;
         u64 Lp[W];
 #pragma unroll
         for (int w = 0; w < W; w++) Lp[w] = __ldg(fv.masks + (size_t)w * F + ii);
@@ -1157,6 +1159,14 @@ static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, 
   ta.rows_pb = (int)(tiles * TJ);
   ta.tiles = (int)tiles;
   ta.ctr_stride = (int)tiles;
+  ta.cw = 32;
+  if (single_cta && f->cur_objective == REMAT_MINIMIZE) {
+    // one CTA walks the level: chunks narrow enough that every warp gets some,
+    // since a predecessor's items stay with the warp that tested it and
+    // minimize frontiers run to hundreds of entries (maximize frontiers hold a
+    // few: wide chunks are cheaper there)
+    ta.cw = (int)std::max<long long>(4, std::min<long long>(32, j0 / (2 * kWarps)));
+  }
   ta.ctr = f->ctr.p;  // [nb][tiles] chunk counters + [nb][tiles] done counters, all zero
   if ((size_t)2 * nb * tiles > f->ctr_cap)
     return fail(REMAT_ERR_INTERNAL, "tile counter capacity exceeded");

@@ -9,7 +9,7 @@ for rep in range(3):
     print("C1 build", round((t1 - t0) * 1e3, 3), "ms solve", round((t2 - t1) * 1e3, 3), "ms", s.timings(), p.stats)
     s.close()
 g = named_graph("densenet161")
-for rep in range(2):
+for rep in range(4):
     s = Solver(g, "pruned"); t1 = time.perf_counter()
     b, p = s.min_feasible_budget("maximize"); t2 = time.perf_counter()
     print("C3 search", round((t2 - t1) * 1e3, 3), "ms", s.timings())
