@@ -371,7 +371,7 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
   remat_graph_s* g = f->g;
   int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;
-  const int K = std::max(1, std::min(probes_per_round, 64));
+  const int K = std::max(1, std::min(probes_per_round, 256));
   const int n = g->n, W = g->W;
   const size_t rows = (size_t)(n + 1);
   // feasibility is monotone in the budget; 2·M(V) always admits the
@@ -383,14 +383,12 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
   std::vector<int64_t> bstage(rows);
   long long probes = 0, ptrans = 0;
   std::vector<remat_plan_info> pinfo;
-  std::vector<uint64_t> pchain, pcached;
-  std::vector<int64_t> pstage;
-  auto take = [&](int idx) {
+  // a round returns only the probes' figures; the rows of the plan that
+  // becomes the new upper bound are fetched from the device alone
+  auto take = [&](int idx) -> int {
     best = pinfo[idx];
-    std::memcpy(bchain.data(), pchain.data() + idx * rows * W, rows * W * 8);
-    std::memcpy(bcached.data(), pcached.data() + idx * rows * W, rows * W * 8);
-    std::memcpy(bstage.data(), pstage.data() + idx * rows, rows * 8);
     have = true;
+    return plan_rows(f, idx, (u64*)bchain.data(), (u64*)bcached.data(), (long long*)bstage.data());
   };
   while (hi - lo > 1) {
     std::vector<int64_t> probe;
@@ -401,11 +399,7 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
     if (probe.empty()) probe.push_back(lo + (hi - lo) / 2);
     const int nb = (int)probe.size();
     pinfo.assign(nb, remat_plan_info{});
-    pchain.assign(nb * rows * W, 0);
-    pcached.assign(nb * rows * W, 0);
-    pstage.assign(nb * rows, 0);
-    rc = remat_solve(f, probe.data(), nb, objective, pinfo.data(), pchain.data(), pcached.data(),
-                     pstage.data());
+    rc = remat_solve(f, probe.data(), nb, objective, pinfo.data(), nullptr, nullptr, nullptr);
     if (rc < 0) return rc;
     probes += nb;
     int first_ok = -1;
@@ -415,7 +409,7 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
     }
     if (first_ok >= 0) {
       hi = probe[first_ok];
-      take(first_ok);
+      if ((rc = take(first_ok)) < 0) return rc;
       if (first_ok > 0) lo = probe[first_ok - 1];
     } else {
       lo = probe.back();
@@ -424,17 +418,13 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
   if (!have) {
     int64_t b = hi;
     pinfo.assign(1, remat_plan_info{});
-    pchain.assign(rows * W, 0);
-    pcached.assign(rows * W, 0);
-    pstage.assign(rows, 0);
-    rc = remat_solve(f, &b, 1, objective, pinfo.data(), pchain.data(), pcached.data(),
-                     pstage.data());
+    rc = remat_solve(f, &b, 1, objective, pinfo.data(), nullptr, nullptr, nullptr);
     if (rc < 0) return rc;
     probes += 1;
     ptrans += pinfo[0].stats.transitions;
     if (pinfo[0].status != REMAT_OK)
       return fail(REMAT_ERR_INTERNAL, "internal error: single-segment plan must fit 2*M(V)");
-    take(0);
+    if ((rc = take(0)) < 0) return rc;
   }
   *b_min = hi;
   *info = best;

@@ -260,6 +260,10 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 int solve_begin(remat_family_s* f, const std::vector<long long>& budgets, int objective);
 int solve_level(remat_family_s* f, int lvl, long long lo, long long hi);
 int solve_levels(remat_family_s* f, const std::vector<int>& lvls);  // full ranges, batched
+// rows (chain, cached, stage memory; n+1 each, unpadded words) of budget b of
+// the last solve, still on the device
+int plan_rows(remat_family_s* f, int b, u64* chain_masks, u64* cached_masks,
+              long long* stage_memory);
 int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                  long long* stage_memory);
 int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,

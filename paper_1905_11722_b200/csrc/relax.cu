@@ -1424,6 +1424,28 @@ int solve_finish(remat_family_s* f, remat_plan_info* info, u64* chain_masks, u64
   });
 }
 
+int plan_rows(remat_family_s* f, int b, u64* chain_masks, u64* cached_masks,
+              long long* stage_memory) {
+  remat_graph_s* g = f->g;
+  const int n = g->n, Wp = g->Wp, Wu = g->W;
+  const size_t rows = (size_t)(n + 1);
+  std::vector<u64> hc(rows * Wp), hk(rows * Wp);
+  cudaStream_t s = g->stream;
+  RM_CUDA(cudaMemcpyAsync(hc.data(), f->chain_out.p + (size_t)b * rows * Wp, hc.size() * 8,
+                          cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaMemcpyAsync(hk.data(), f->cached_out.p + (size_t)b * rows * Wp, hk.size() * 8,
+                          cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaMemcpyAsync(stage_memory, f->stage_out.p + (size_t)b * rows, rows * 8,
+                          cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  for (size_t q = 0; q < rows; q++)
+    for (int w = 0; w < Wu; w++) {
+      chain_masks[q * Wu + w] = hc[q * Wp + w];
+      cached_masks[q * Wu + w] = hk[q * Wp + w];
+    }
+  return REMAT_OK;
+}
+
 int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int objective,
                 remat_plan_info* info, u64* chain_masks, u64* cached_masks,
                 long long* stage_memory) {

@@ -133,9 +133,9 @@ class Solver:
         if objective not in OBJECTIVES:
             raise ValueError(f"objective must be one of {OBJECTIVES}, got {objective!r}")
         if probes_per_round is None:
-            # small families solve one budget per CTA: a round of 48 probes costs
+            # small families solve one budget per CTA: a round of 144 probes costs
             # what one probe does, so the search takes few, wide rounds
-            probes_per_round = 48 if self.dev.size <= SMALL_FAMILY else 8
+            probes_per_round = 144 if self.dev.size <= SMALL_FAMILY else 8
         t0 = time.perf_counter()
         bmin, raw, search = self.dev.min_feasible_budget(objective, probes_per_round)
         wall = time.perf_counter() - t0
