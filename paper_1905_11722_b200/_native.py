@@ -333,8 +333,15 @@ class DeviceFamily:
                 np.zeros((nb, rows, self.dg.w), dtype=np.uint64),
                 np.zeros((nb, rows), dtype=np.int64))
 
+    MAX_BATCH = 256  # budgets per device solve (DP tables scale with the batch)
+
     def solve(self, budgets: list[int], objective: str):
         """Batched dp over ``budgets``: list of (PlanInfo, chain, cached, stages)."""
+        if len(budgets) > self.MAX_BATCH:
+            out = []
+            for k in range(0, len(budgets), self.MAX_BATCH):
+                out += self.solve(budgets[k:k + self.MAX_BATCH], objective)
+            return out
         nb = len(budgets)
         b = np.asarray([min(int(x), 2**62) for x in budgets], dtype=np.int64)
         infos = (PlanInfo * nb)()
