@@ -337,6 +337,8 @@ class DeviceFamily:
 
     def solve(self, budgets: list[int], objective: str):
         """Batched dp over ``budgets``: list of (PlanInfo, chain, cached, stages)."""
+        if not budgets:
+            return []
         if len(budgets) > self.MAX_BATCH:
             out = []
             for k in range(0, len(budgets), self.MAX_BATCH):
