@@ -43,6 +43,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -1145,12 +1146,19 @@ static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, 
   ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
   if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
   const long long tiles = (width + TJ - 1) / TJ;
+  // narrower predecessor chunks where even one target per tile leaves the GPU
+  // short of (tile, chunk) tasks (chain-like levels: one target, hundreds of
+  // predecessors with long frontiers)
+  int cw = 32;
+  if (!single_cta)
+    while (cw > 4 && tiles * ((j0 + cw - 1) / cw) * nb < want / 4) cw /= 2;
+  const long long nchw = (j0 + cw - 1) / cw;
   // split the predecessor scan across CTAs when the level alone cannot fill
   // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
   long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
   if (max_vctas > 0) splits = max_vctas / (tiles * nb);  // persistent: one round per block
   if (single_cta) splits = 1;
-  splits = std::max(1LL, std::min(splits, nch / kWarps));
+  splits = std::max(1LL, std::min(splits, nchw / kWarps));
   ta.jbase = lo;
   ta.pend = j0;
   ta.width = (int)width;
@@ -1159,7 +1167,7 @@ static int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, 
   ta.rows_pb = (int)(tiles * TJ);
   ta.tiles = (int)tiles;
   ta.ctr_stride = (int)tiles;
-  ta.cw = 32;
+  ta.cw = cw;
   if (single_cta && f->cur_objective == REMAT_MINIMIZE) {
     // one CTA walks the level: chunks narrow enough that every warp gets some,
     // since a predecessor's items stay with the warp that tested it and
@@ -1453,7 +1461,15 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
   if (rc < 0) return rc;
   // a small family (pruned families, chain-like lattices) runs whole in one
   // CTA per budget
-  if (f->F <= kSmallFamily) {
+  static const long long small_family = [] {
+    const char* e = getenv("REMAT_SMALL_FAMILY");  // tuning / test hook
+    return e ? atoll(e) : kSmallFamily;
+  }();
+  // one CTA per budget pays off when the batch itself fills the GPU and the
+  // frontiers are short (maximize keeps a few entries per cell);
+  // a single budget, or long minimize frontiers, spread each level over CTAs
+  const bool small_ok = objective == REMAT_MAXIMIZE ? budgets.size() >= 16 : budgets.size() >= 48;
+  if (f->F <= small_family && small_ok) {
     if ((rc = solve_small(f)) < 0) return rc;
     if (rc == REMAT_OK) return solve_finish(f, info, chain_masks, cached_masks, stage_memory);
   }

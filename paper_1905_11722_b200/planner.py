@@ -133,9 +133,12 @@ class Solver:
         if objective not in OBJECTIVES:
             raise ValueError(f"objective must be one of {OBJECTIVES}, got {objective!r}")
         if probes_per_round is None:
-            # small families solve one budget per CTA: a round of 144 probes costs
-            # what one probe does, so the search takes few, wide rounds
-            probes_per_round = 144 if self.dev.size <= SMALL_FAMILY else 8
+            # small families: maximize rounds run one budget per CTA (144 probes
+            # cost what one does); minimize rounds spread every probe over CTAs
+            if self.dev.size <= SMALL_FAMILY:
+                probes_per_round = 144 if objective == "maximize" else 32
+            else:
+                probes_per_round = 8
         t0 = time.perf_counter()
         bmin, raw, search = self.dev.min_feasible_budget(objective, probes_per_round)
         wall = time.perf_counter() - t0
