@@ -285,7 +285,32 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
     bs[b] = std::min<long long>(budgets[b], 2 * g->MV);
   }
   int rc;
-  if ((rc = ensure_foff(f)) < 0 || (rc = solve_begin(f, bs, objective)) < 0) return rc;
+  if ((rc = ensure_foff(f)) < 0) return rc;
+  if (c->world > 1) {
+    // every rank must hold the same family and solve the same budgets: one
+    // all-gather of a small header checks it before any level is exchanged
+    const int HW = 6;
+    long long mine[HW] = {f->F, f->slots, (long long)g->n, (long long)f->narrow, (long long)nb,
+                          (long long)objective};
+    for (int b = 0; b < nb; b++) mine[4] = mine[4] * 1000003LL + bs[b];
+    if ((rc = c->send.ensure(sizeof mine)) < 0 || (rc = c->recv.ensure(sizeof mine * c->world)) < 0)
+      return rc;
+    RM_CUDA(cudaMemcpyAsync(c->send.p, mine, sizeof mine, cudaMemcpyHostToDevice, g->stream));
+    ncclResult_t r = api->allGather(c->send.p, c->recv.p, sizeof mine, ncclUint8, c->comm,
+                                    g->stream);
+    if (r != ncclSuccess)
+      return fail(REMAT_ERR_CUDA, std::string("ncclAllGather: ") + api->errorString(r));
+    std::vector<long long> all((size_t)HW * c->world);
+    RM_CUDA(cudaMemcpyAsync(all.data(), c->recv.p, sizeof mine * c->world, cudaMemcpyDeviceToHost,
+                            g->stream));
+    RM_CUDA(cudaStreamSynchronize(g->stream));
+    for (int q = 0; q < c->world; q++)
+      for (int k = 0; k < HW; k++)
+        if (all[(size_t)q * HW + k] != mine[k])
+          return fail(REMAT_ERR_VALUE, "level-sharded ranks disagree on the family or budgets (rank " +
+                                           std::to_string(q) + ")");
+  }
+  if ((rc = solve_begin(f, bs, objective)) < 0) return rc;
   SegList sl;
   const char* fx = getenv("REMAT_SHARD_EXCHANGE");
   const bool force_exchange = fx && fx[0] == '1';
