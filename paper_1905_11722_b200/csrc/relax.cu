@@ -39,6 +39,7 @@
 // with Σ_i|frontier_i| and the comparable-pair counts accumulated during the
 // scan these are exactly table_entries, states_visited and transitions
 // (Appendix A.3).
+//
 // The kernels and the per-width drivers live in relax_impl.cuh and are
 // instantiated one bitset width per translation unit (relax_w*.cu); this file
 // holds the width dispatch and the batch driver.

@@ -21,10 +21,10 @@ constexpr int kSmallF = 4;       // frontier entries kept in registers (small-fr
 
 // One relaxable (predecessor, target) pair of a warp's current group.
 struct __align__(16) PairQN {  // narrow: one LDS.128
-  int base;       // entry index (within the budget's table) of item 0, minus its item offset
+  int base;       // shared-window byte address of row slot dt_ij of the target (shared rows)
   unsigned cap;   // B − fixed_ij: an entry passes the budget test iff m <= cap
   unsigned kb;    // (dm_ij << IB) | i: key = (m << IB) + kb
-  int dtr;        // target row offset in the tile + dt_ij
+  int dtr;        // target row offset in the tile + dt_ij (element index, global rows)
 };
 struct __align__(16) PairQW {
   long long base;
@@ -188,26 +188,6 @@ __device__ __forceinline__ void relax_smem2(unsigned a0, unsigned k0, bool ok0, 
       "@q0 red.shared.min.u32 [%0], %1;\n\t"
       "@q1 red.shared.min.u32 [%3], %4;\n\t}"
       ::"r"(a0), "r"(k0), "r"((unsigned)ok0), "r"(a1), "r"(k1), "r"((unsigned)ok1));
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_min_all(T v) {
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) {
-    T o = __shfl_xor_sync(kFull, v, m);
-    v = o < v ? o : v;
-  }
-  return v;
-}
-
-template <typename T>
-__device__ __forceinline__ T warp_max_all(T v) {
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) {
-    T o = __shfl_xor_sync(kFull, v, m);
-    v = o > v ? o : v;
-  }
-  return v;
 }
 
 template <typename T>
