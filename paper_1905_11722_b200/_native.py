@@ -16,7 +16,9 @@ import numpy as np
 
 from .graph import GraphError, pack_graph
 
-LIB_PATH = Path(__file__).resolve().parent / "libremat_b200.so"
+# REMAT_B200_LIB: an alternative build of the same library (A/B runs of kernel variants)
+LIB_PATH = Path(os.environ.get("REMAT_B200_LIB") or
+                Path(__file__).resolve().parent / "libremat_b200.so")
 
 OK, INFEASIBLE = 0, 1
 ERR_VALUE, ERR_LATTICE, ERR_CUDA, ERR_NOMEM, ERR_INTERNAL, ERR_RANGE, ERR_SIM = (

@@ -244,6 +244,7 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
     }
   g->hT.assign(compute_costs, compute_costs + n);
   g->hM.assign(memory_costs, memory_costs + n);
+  g->t_uniform = std::all_of(g->hT.begin(), g->hT.end(), [&](long long t) { return t == g->hT[0]; });
   std::vector<u64> cls;
   std::vector<long long> coef;
   g->cls_enabled = joint_classes(g->hT, g->hM, n, Wp, cls, coef);

@@ -191,6 +191,7 @@ struct remat_graph_s {
   remat::DevBuf<u64> cls;
   remat::DevBuf<long long> coef;
   std::vector<long long> hT, hM;
+  int t_uniform = 0;  // every T_v equal: candidates of a warp collide on few row slots
   // evaluate / simulate scratch
   remat::DevBuf<u64> chain_buf, bound_buf, cached_buf;
   remat::DevBuf<long long> terms_buf, eval_out, stage_buf;

@@ -104,6 +104,7 @@ struct TileArgs {
   unsigned* ctr;    // [nb][ctr_stride] next predecessor chunk of the tile (left zero)
   int tiles;
   int cw;           // predecessors per chunk (<= 32)
+  int probe;        // small-frontier path: probe a slot before its RED (uniform T_v)
   int ctr_stride;   // counters per budget: tiles, or the widest level when budgets run
                     // through the levels independently (k_solve_small)
   int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_coef, off_tacc, off_pairs, off_q, off_qs, off_rows;
@@ -160,9 +161,42 @@ __device__ __forceinline__ void key_min(u64* p, u64 key, bool smem) {
 
 // One candidate into a shared-memory row: row[t2] = min(row[t2], key) if `ok`.
 // Every candidate's slot t2 = t + dt_ij <= T(L_j) is inside the row even when
-// the budget test fails, so the probe is unconditional and the update a
-// predicated RED (no branch, no reconvergence); only ~1 in 6 candidates
-// improves its slot.
+// the budget test fails, so the slot address is always valid.
+// Item path (long frontiers): every candidate issues its RED unconditionally
+// (INF when it fails the budget test).  A probe-then-predicated-RED costs a
+// shared load, a compare and — since ptxas lowers a predicated shared atomic
+// to a branch — a reconvergence region per candidate; the bare RED is cheaper
+// whenever candidates of a warp step rarely collide on one slot
+// (U-Net c=8 relaxation: 17.3 -> 15.5 ms).
+__device__ __forceinline__ void red_smem(unsigned a, unsigned key, bool ok) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(ok ? key : 0xffffffffu));
+}
+// All pairs [qp, qe) of one item (entry t, m; mk = m << IB, t4 = 4t), four
+// records per step so four LDS.128 are in flight (U-Net c=8: 4 -> 2 per step
+// costs 0.6 %, 1 per step 4 %).
+__device__ __forceinline__ void red_pairs(const PairQN* qp, const PairQN* qe, unsigned t4,
+                                          unsigned mk, unsigned m) {
+  for (; qp + 3 < qe; qp += 4) {
+    const PairQN p0 = Traits<true>::lds(qp), p1 = Traits<true>::lds(qp + 1);
+    const PairQN p2 = Traits<true>::lds(qp + 2), p3 = Traits<true>::lds(qp + 3);
+    red_smem(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap);
+    red_smem(t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
+    red_smem(t4 + (unsigned)p2.base, mk + p2.kb, m <= p2.cap);
+    red_smem(t4 + (unsigned)p3.base, mk + p3.kb, m <= p3.cap);
+  }
+  for (; qp + 1 < qe; qp += 2) {
+    const PairQN p0 = Traits<true>::lds(qp), p1 = Traits<true>::lds(qp + 1);
+    red_smem(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap);
+    red_smem(t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
+  }
+  if (qp < qe) {
+    const PairQN p = Traits<true>::lds(qp);
+    red_smem(t4 + (unsigned)p.base, mk + p.kb, m <= p.cap);
+  }
+}
+// Small-frontier path when every T_v is equal (few distinct slots, the lanes
+// of a warp collide on them and same-address REDs serialise): probe first, so
+// a losing candidate issues no atomic.
 __device__ __forceinline__ void relax_smem(unsigned a, unsigned key, bool ok) {
   asm volatile(
       "{\n\t.reg .pred o, q;\n\t.reg .u32 c;\n\t"
@@ -171,23 +205,6 @@ __device__ __forceinline__ void relax_smem(unsigned a, unsigned key, bool ok) {
       "setp.lt.and.u32 q, %1, c, o;\n\t"
       "@q red.shared.min.u32 [%0], %1;\n\t}"
       ::"r"(a), "r"(key), "r"((unsigned)ok));
-}
-
-// Two candidates at once (two rows of the tile, so never the same slot): both
-// probes are issued before either update.
-__device__ __forceinline__ void relax_smem2(unsigned a0, unsigned k0, bool ok0, unsigned a1,
-                                            unsigned k1, bool ok1) {
-  asm volatile(
-      "{\n\t.reg .pred o0, o1, q0, q1;\n\t.reg .u32 c0, c1;\n\t"
-      "ld.shared.u32 c0, [%0];\n\t"
-      "ld.shared.u32 c1, [%3];\n\t"
-      "setp.ne.u32 o0, %2, 0;\n\t"
-      "setp.ne.u32 o1, %5, 0;\n\t"
-      "setp.lt.and.u32 q0, %1, c0, o0;\n\t"
-      "setp.lt.and.u32 q1, %4, c1, o1;\n\t"
-      "@q0 red.shared.min.u32 [%0], %1;\n\t"
-      "@q1 red.shared.min.u32 [%3], %4;\n\t}"
-      ::"r"(a0), "r"(k0), "r"((unsigned)ok0), "r"(a1), "r"(k1), "r"((unsigned)ok1));
 }
 
 template <typename T>
@@ -471,7 +488,10 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           const Key key = ((Key)em[e] << IB) + (Key)q.kb;
           if constexpr (NARROW) {
             if (srow) {
-              relax_smem((unsigned)q.base + 4u * et[e], key, em[e] <= q.cap);
+              if (ta.probe)
+                relax_smem((unsigned)q.base + 4u * et[e], key, em[e] <= q.cap);
+              else
+                red_smem((unsigned)q.base + 4u * et[e], key, em[e] <= q.cap);
               continue;
             }
           }
@@ -554,9 +574,9 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     // Item e belongs to the last live predecessor starting at or before e:
     // per 32-item step one REDUX.OR gathers the predecessor starts inside the
     // step and a popcount ranks each lane among them.  One entry load then
-    // feeds every budget-feasible target of that predecessor in the tile
-    // (rows are addressed through the shared window directly when they live
-    // in shared memory, so the row probe is an LDS and the update an ATOMS).
+    // feeds every target of that predecessor in the tile (rows are addressed
+    // through the shared window directly when they live in shared memory, so
+    // each candidate is one ATOMS.MIN).
     const unsigned le = lt | (1u << lane);
     // smem: rows addressed as 32-bit shared-window offsets; global: pointers
     auto relax_items = [&](Key* __restrict__ rw, const unsigned rs, const bool smem) {
@@ -602,15 +622,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           const Q* qp = wq + rec.q0;
           if constexpr (NARROW) {
             if (smem) {
-              for (; qp + 1 < qe; qp += 2) {
-                const Q p0 = Traits<NARROW>::lds(qp), p1 = Traits<NARROW>::lds(qp + 1);
-                relax_smem2(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap,
-                            t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
-              }
-              if (qp < qe) {
-                const Q p = Traits<NARROW>::lds(qp);
-                relax_smem(t4 + (unsigned)p.base, mk + p.kb, m <= p.cap);
-              }
+              red_pairs(qp, qe, t4, mk, m);
               qp = qe;
             }
           }
@@ -671,15 +683,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         const Q* qp = wq + x.rec.q0;
         if constexpr (NARROW) {
           if (smem) {
-            for (; qp + 1 < qe; qp += 2) {
-              const Q p0 = Traits<NARROW>::lds(qp), p1 = Traits<NARROW>::lds(qp + 1);
-              relax_smem2(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap,
-                          t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
-            }
-            if (qp < qe) {
-              const Q p = Traits<NARROW>::lds(qp);
-              relax_smem(t4 + (unsigned)p.base, mk + p.kb, m <= p.cap);
-            }
+            red_pairs(qp, qe, t4, mk, m);
             return;
           }
         }
@@ -1107,6 +1111,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   ta.tiles = (int)tiles;
   ta.ctr_stride = (int)tiles;
   ta.cw = cw;
+  ta.probe = g->t_uniform;
   if (single_cta && f->cur_objective == REMAT_MINIMIZE) {
     // one CTA walks the level: chunks narrow enough that every warp gets some,
     // since a predecessor's items stay with the warp that tested it and
