@@ -426,6 +426,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   // + warp), later ones come from the counter, offset past the static ones
   const long long nstatic = (long long)splits * kWarps;
   auto next_chunk = [&]() {
+    if (nstatic >= nch) return nch;  // the static chunks covered the range
     unsigned got = 0;
     if (lane == 0) got = atomicAdd(ctr, 1u);
     return nstatic + (long long)__shfl_sync(kFull, got, 0);
@@ -1122,7 +1123,8 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
   if (max_vctas > 0) splits = max_vctas / (tiles * nb);  // persistent: one round per block
   if (single_cta) splits = 1;
-  splits = std::max(1LL, std::min(splits, nchw / kWarps));
+  // (rounded up: every chunk of a narrow level is some warp's static first one)
+  splits = std::max(1LL, std::min(splits, (nchw + kWarps - 1) / kWarps));
   ta.jbase = lo;
   ta.pend = j0;
   ta.width = (int)width;
