@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <utility>
 
 #include "device.cuh"
 
@@ -298,43 +299,31 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
 // COH: the table being read was written earlier in the SAME launch (persistent
 // multi-level kernel) — frontier entries and per-member records are then read
 // through L2 (ld.cg), never the non-coherent path.
-template <int W, bool NARROW, bool COH, bool DUAL = false>
-__device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView& g,
-                                           const ClassView& cv, const DpView& dp,
-                                           const TileArgs& ta, const int vbx, const int b,
-                                           const int nb, unsigned char* sm) {
+// Shared-memory set-up of a tile: the targets' sets and scalars, empty rows,
+// the weight-class masks.  Reads family constants only, so the persistent
+// kernel runs it for the next level before the grid barrier.
+__shared__ int s_relax_worked;
+
+template <int W, bool NARROW>
+__device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView& cv,
+                                           const TileArgs& ta, const int vbx, unsigned char* sm) {
   using Key = typename Traits<NARROW>::Key;
-  using E = typename Traits<NARROW>::E;
-  using Q = typename Traits<NARROW>::Q;
-  using MT = typename Traits<NARROW>::M;
   constexpr Key INF = Traits<NARROW>::INF;
-  __shared__ int s_worked;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned lt = (1u << lane) - 1;
-  const int TJ = ta.TJ, R = ta.R, splits = ta.splits;
-  if (tid == 0) s_worked = 0;
+  const int tid = threadIdx.x;
+  const int TJ = ta.TJ, R = ta.R;
   const long long F = fv.F;
-  const int tile = vbx / splits;
-  const long long j0 = ta.jbase + (long long)tile * TJ;
+  const long long j0 = ta.jbase + (long long)(vbx / ta.splits) * TJ;
   const int ntj = (int)min((long long)TJ, ta.jbase + ta.width - j0);
-
-  u64* tL = reinterpret_cast<u64*>(sm + ta.off_tL);         // [TJ][W]
-  u64* tB = reinterpret_cast<u64*>(sm + ta.off_tB);         // [TJ][W]
-  long long* tc = reinterpret_cast<long long*>(sm + ta.off_tc);  // [TJ][4]
-  int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);     // [TJ]
-  u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
-  long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);  // [K][2]
-  u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
-  unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
-  Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * 32 * TJ;  // feasible pairs of a chunk
-  PredRec* wrec = reinterpret_cast<PredRec*>(sm + ta.off_qs) + warp * 32;  // live predecessors
-  int* wpc = reinterpret_cast<int*>(sm + ta.off_qs + kWarps * 32 * 16) + warp * 32;
-  Key* grow_t = ta.grow ? reinterpret_cast<Key*>(ta.grow) +
-                              ((size_t)b * ta.rows_pb + (size_t)tile * TJ) * R
-                        : nullptr;
-  Key* rows = ta.smem_rows ? reinterpret_cast<Key*>(sm + ta.off_rows) : grow_t;
+  u64* tL = reinterpret_cast<u64*>(sm + ta.off_tL);
+  u64* tB = reinterpret_cast<u64*>(sm + ta.off_tB);
+  long long* tc = reinterpret_cast<long long*>(sm + ta.off_tc);
+  int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);
+  u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);
+  long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);
+  u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);
+  Key* rows = reinterpret_cast<Key*>(sm + ta.off_rows);
   const bool srow = ta.smem_rows;
-
+  if (tid == 0) s_relax_worked = 0;
   for (int e = tid; e < ntj * W; e += kThreads) {
     const int jt = e / W, w = e - jt * W;
     tL[e] = fv.masks[(size_t)w * F + j0 + jt];
@@ -366,6 +355,48 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     tcls[jt] = ta.cls && K * W < bc;
   }
   __syncthreads();
+
+}
+
+template <int W, bool NARROW, bool COH, bool DUAL = false>
+__device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView& g,
+                                           const ClassView& cv, const DpView& dp,
+                                           const TileArgs& ta, const int vbx, const int b,
+                                           const int nb, unsigned char* sm,
+                                           const bool presetup = false) {
+  using Key = typename Traits<NARROW>::Key;
+  using E = typename Traits<NARROW>::E;
+  using Q = typename Traits<NARROW>::Q;
+  using MT = typename Traits<NARROW>::M;
+  constexpr Key INF = Traits<NARROW>::INF;
+  int& s_worked = s_relax_worked;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = (1u << lane) - 1;
+  const int TJ = ta.TJ, R = ta.R, splits = ta.splits;
+  const long long F = fv.F;
+  const int tile = vbx / splits;
+  const long long j0 = ta.jbase + (long long)tile * TJ;
+  const int ntj = (int)min((long long)TJ, ta.jbase + ta.width - j0);
+
+  u64* tL = reinterpret_cast<u64*>(sm + ta.off_tL);         // [TJ][W]
+  u64* tB = reinterpret_cast<u64*>(sm + ta.off_tB);         // [TJ][W]
+  long long* tc = reinterpret_cast<long long*>(sm + ta.off_tc);  // [TJ][4]
+  int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);     // [TJ]
+  u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
+  long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);  // [K][2]
+  u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
+  unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
+  Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * 32 * TJ;  // feasible pairs of a chunk
+  PredRec* wrec = reinterpret_cast<PredRec*>(sm + ta.off_qs) + warp * 32;  // live predecessors
+  int* wpc = reinterpret_cast<int*>(sm + ta.off_qs + kWarps * 32 * 16) + warp * 32;
+  Key* grow_t = ta.grow ? reinterpret_cast<Key*>(ta.grow) +
+                              ((size_t)b * ta.rows_pb + (size_t)tile * TJ) * R
+                        : nullptr;
+  Key* rows = ta.smem_rows ? reinterpret_cast<Key*>(sm + ta.off_rows) : grow_t;
+  const bool srow = ta.smem_rows;
+
+  if (!presetup) tile_setup<W, NARROW>(fv, cv, ta, vbx, sm);
+  const int K = cv.K;
 
   const long long B = dp.budgets[b];
   const int IB = dp.IB;
@@ -847,14 +878,34 @@ __global__ void __launch_bounds__(kThreads)
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char sm[];
+  // the block's first tile of each level is set up between its arrival at
+  // the barrier that ends the previous level and the wait (the loads overlap
+  // the other blocks' finish)
+  bool pre = false;
+  if (nlev > 0 && blockIdx.x < levels[0].tiles * levels[0].splits * nb) {
+    tile_setup<W, NARROW>(fv, cv, levels[0], blockIdx.x % (levels[0].tiles * levels[0].splits), sm);
+    pre = true;
+  }
   for (int l = 0; l < nlev; l++) {
     const TileArgs ta = levels[l];
     const int per = ta.tiles * ta.splits;
     for (int v = blockIdx.x; v < per * nb; v += gridDim.x) {
-      relax_body<W, NARROW, true>(fv, g, cv, dp, ta, v % per, v / per, nb, sm);
+      relax_body<W, NARROW, true>(fv, g, cv, dp, ta, v % per, v / per, nb, sm,
+                                  pre && v == (int)blockIdx.x);
       __syncthreads();
     }
-    grid.sync();
+    // split barrier: arrive, set up the next level's first tile, then wait
+    auto token = grid.barrier_arrive();
+    pre = false;
+    if (l + 1 < nlev) {
+      const TileArgs& tn = levels[l + 1];
+      const int pn = tn.tiles * tn.splits;
+      if ((int)blockIdx.x < pn * nb) {
+        tile_setup<W, NARROW>(fv, cv, tn, blockIdx.x % pn, sm);
+        pre = true;
+      }
+    }
+    grid.barrier_wait(std::move(token));
   }
 }
 
