@@ -1166,8 +1166,14 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   // short of (tile, chunk) tasks (chain-like levels: one target, hundreds of
   // predecessors with long frontiers)
   int cw = 32;
-  if (!single_cta)
-    while (cw > 4 && tiles * ((j0 + cw - 1) / cw) * nb < want / 4) cw /= 2;
+  if (!single_cta) {
+    // long frontiers (minimize, varied T_v: hundreds of entries per cell)
+    // go down to one predecessor per warp, so a chain-like level's items
+    // spread over the most CTAs (C1 3.8 -> 3.2 ms); short ones (maximize,
+    // uniform T_v) keep >= 4 per chunk
+    const int mincw = f->cur_objective == REMAT_MINIMIZE && !g->t_uniform ? 1 : 4;
+    while (cw > mincw && tiles * ((j0 + cw - 1) / cw) * nb < want / 4) cw /= 2;
+  }
   const long long nchw = (j0 + cw - 1) / cw;
   // split the predecessor scan across CTAs when the level alone cannot fill
   // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
