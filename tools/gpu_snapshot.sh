@@ -11,5 +11,5 @@ timeout 600 python bench.py --workload random-dag --edge-prob 0.3 --no-cpu > gpu
 timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 bash tools/gpu_launches.sh
 bash tools/gpu_traffic.sh unet
-bash tools/gpu_prof.sh k_relax_tile 40
+bash tools/gpu_prof.sh k_relax_tile 14
 tail -2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; head -c 600 gpurun_out/bench.json; echo
