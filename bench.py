@@ -356,6 +356,10 @@ def run_ours(args, world, rank, local):
         rec = json.loads(prof.read_text()).get(name)
         if rec:
             traffic = rec["dram_bytes_per_launch"]
+    issue = None
+    prof_i = ROOT / "profiles" / "relax_issue.json"
+    if prof_i.exists():  # ncu capture of the heaviest launch + measured issue peak
+        issue = json.loads(prof_i.read_text()).get(name)
     line = {
         "metric": "exact-DP transitions/s (end-to-end solve)",
         "value": value, "unit": "transitions/s", "n_gpus": world, "steps": args.steps,
@@ -379,7 +383,9 @@ def run_ours(args, world, rank, local):
                      "note": ("achieved = SURVEY 8(d) algorithmic bytes 12X+(16W+16)P+16E of the "
                               "relaxation / its device time; the table is L2-resident (traffic = "
                               "measured DRAM bytes per launch), so the binding resource is SM "
-                              "issue on shared-memory row probes, see profiles/")},
+                              "issue (see `issue`: executed IPC of the heaviest launch against "
+                              "the measured 4-slot issue peak, tools/micro/pipes.cu)"),
+                     "issue": issue},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s},
