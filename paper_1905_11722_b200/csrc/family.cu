@@ -424,6 +424,101 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 // host drivers
 // ---------------------------------------------------------------------------
 
+// Narrow levels (a few dozen members: the long tails of deep lattices, C5)
+// are walked by ONE block with members in shared memory and CTA barriers
+// only: a grid barrier plus the L2 round trips of a grid step cost more than
+// the whole level's candidate checks.  Block 0 ranks, scatters and expands
+// level after level until a level gets wide (or V is reached) and returns the
+// level to resume the grid walk at (-1: the lattice overflowed, status set).
+// Level k+1 is also written to U[(k+1) % 3], where the grid walk expects it.
+template <int W>
+__device__ __noinline__ int enum_narrow_run(const u64* __restrict__ preds, int n, long long cap, long long fcap,
+                               u64* __restrict__ fam, u64* __restrict__ U, long long ucap,
+                               long long* __restrict__ ctr, long long* __restrict__ ls,
+                               int* __restrict__ status, int k, long long base, int ncap,
+                               long long work_cap, u64* __restrict__ sm) {
+  __shared__ int s_cnt;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nch = (n + 31) / 32;
+  u64* cur = sm;
+  u64* nxt = sm + (size_t)ncap * 2 * W;
+  long long N = *((volatile long long*)(ctr + k));
+  {
+    const u64* g = U + (size_t)(k % 3) * ucap * 2 * W;
+    for (long long e = tid; e < N * 2 * W; e += blockDim.x) cur[e] = g[e];
+  }
+  __syncthreads();
+  while (true) {
+    if (base + N > cap || base + N > fcap) {
+      if (tid == 0) status[0] = base + N > cap ? 1 : 2;
+      return -1;
+    }
+    if (tid == 0) ls[k] = base;
+    // rank (all masks of a level are distinct) and scatter level k
+    if (tid < N) {
+      const u64* me = cur + (size_t)tid * 2 * W;
+      long long r = 0;
+      for (int q = 0; q < N; q++) r += mask_less<W>(cur + (size_t)q * 2 * W, me);
+#pragma unroll
+      for (int w = 0; w < W; w++) fam[(base + r) * W + w] = me[w];
+    }
+    if (k == n) {  // V has no children; the grid walk only closes ls
+      if (tid == 0) ls[n + 1] = base + N;
+      return n + 1;
+    }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    // canonical children of level k
+    const long long room = min(min(cap, fcap) - base - N, ucap);
+    u64* gn = U + (size_t)((k + 1) % 3) * ucap * 2 * W;
+    for (long long task = warp; task < N * nch; task += blockDim.x >> 5) {
+      const long long p = task / nch;
+      const int v = (int)(task - p * nch) * 32 + lane;
+      u64 L[W], X[W], cx[W];
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        L[w] = cur[p * 2 * W + w];
+        X[w] = cur[p * 2 * W + W + w];
+      }
+      const bool ok = v < n && canonical_child<W>(L, X, v, preds, cx);
+      const unsigned bal = __ballot_sync(kFull, ok);
+      if (!bal) continue;
+      int at0 = 0;
+      if (lane == 0) at0 = atomicAdd(&s_cnt, __popc(bal));
+      at0 = __shfl_sync(kFull, at0, 0);
+      const int at = at0 + __popc(bal & ((1u << lane) - 1));
+      if (ok) {
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+          const u64 cl = L[w] | ((w == (v >> 6)) ? (1ull << (v & 63)) : 0ull);
+          if (at < room) {
+            gn[(size_t)at * 2 * W + w] = cl;
+            gn[(size_t)at * 2 * W + W + w] = cx[w];
+          }
+          if (at < ncap) {
+            nxt[(size_t)at * 2 * W + w] = cl;
+            nxt[(size_t)at * 2 * W + W + w] = cx[w];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const long long N1 = s_cnt;
+    if (tid == 0) ctr[k + 1] = N1;
+    base += N;
+    k++;
+    u64* t = cur;
+    cur = nxt;
+    nxt = t;
+    N = N1;
+    __syncthreads();
+    if (N > ncap || N * n > work_cap) {
+      if (tid == 0) ls[k] = base;
+      return k;  // wide again: the grid walk resumes at level k (in U[k % 3])
+    }
+  }
+}
+
 // K1 as ONE cooperative launch with one grid barrier per level (SURVEY §7
 // hard part 5: n = 516 dependent levels at C5).  Level k's members sit
 // UNSORTED (mask + maximal-element set) in buffer U[k % 3].  Grid step k runs
@@ -437,10 +532,12 @@ int scan_exclusive(const long long* in, long long* out, long long n, cudaStream_
 //   (c) scatter of level k-1 into the family at ls[k-1] + rank, using the
 //       ranks completed in step k-1.
 // Buffers rotate over three slots, so each is written one step after its
-// last reader finished.
+// last reader finished.  Runs of narrow levels go to enum_narrow_run (block 0
+// alone, the others wait at one grid barrier).
 //   ctr[k]    |level k| (ctr[0] = 1: the empty set, pre-set by the host)
 //   status[0] 1 when the lattice exceeds `cap` (LatticeTooLargeError), 2 when
-//             it exceeds the buffers' capacity `fcap` (< cap): grow and rerun
+//             it exceeds the buffers' capacity `fcap` (< cap): grow and rerun;
+//   status[1] the level a narrow run hands back
 template <int W>
 __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds, int n,
                                                   long long cap, long long fcap,
@@ -449,10 +546,12 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
                                                   unsigned* __restrict__ rank,
                                                   long long* __restrict__ ctr,
                                                   long long* __restrict__ ls,
-                                                  int* __restrict__ status) {
+                                                  int* __restrict__ status, int ncap,
+                                                  long long work_cap) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   __shared__ u64 tile[256 * W];
+  extern __shared__ u64 narrow_sm[];  // [2][ncap][2W]
   const int lane = threadIdx.x & 31;
   const long long nwarps = (long long)gridDim.x * 8;
   const long long gw = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -460,23 +559,45 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
   const long long nthreads = (long long)gridDim.x * 256;
   const int nch = (n + 31) / 32;
   long long base = 0, prev_base = 0, prevN = 0;  // ls[k], ls[k-1], |level k-1|
-  for (int k = 0; k <= n + 1; k++) {
-    const long long N = k <= n ? *((volatile long long*)(ctr + k)) : 0;
+  for (int k = 0; k <= n + 1;) {
+    long long N = k <= n ? *((volatile long long*)(ctr + k)) : 0;
     if (base + N > cap || base + N > fcap) {  // uniform: every block read the same counters
       if (blockIdx.x == 0 && threadIdx.x == 0) status[0] = base + N > cap ? 1 : 2;
       return;
     }
+    const unsigned* rkp = rank + (size_t)((k + 2) % 3) * ucap;
+    const u64* prv = U + (size_t)((k + 2) % 3) * ucap * 2 * W;
+    if (k <= n && N <= ncap && N * n <= work_cap) {
+      // narrow run: finish level k-1's scatter here, block 0 takes over
+      for (long long i = gt; i < prevN; i += nthreads) {
+        const long long at = prev_base + rkp[i];
+        const_cast<unsigned*>(rkp)[i] = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) fam[at * W + w] = prv[i * 2 * W + w];
+      }
+      if (blockIdx.x == 0) {
+        const int kr = enum_narrow_run<W>(preds, n, cap, fcap, fam, U, ucap, ctr, ls, status, k,
+                                          base, ncap, work_cap, narrow_sm);
+        if (threadIdx.x == 0) status[1] = kr;
+      }
+      grid.sync();
+      const int kr = *((volatile int*)(status + 1));
+      if (kr < 0) return;
+      base = *((volatile long long*)(ls + kr));
+      prevN = 0;
+      k = kr;
+      if (k > n) break;
+      continue;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0 && k <= n) ls[k] = base;
     const u64* cur = U + (size_t)(k % 3) * ucap * 2 * W;   // [N][2W]
     u64* nxt = U + (size_t)((k + 1) % 3) * ucap * 2 * W;
-    const u64* prv = U + (size_t)((k + 2) % 3) * ucap * 2 * W;
     unsigned* rk = rank + (size_t)(k % 3) * ucap;
-    unsigned* rkp = rank + (size_t)((k + 2) % 3) * ucap;
     const long long room = min(min(cap, fcap) - base - N, ucap);  // children that fit
     // (c) scatter level k-1, leaving its rank slot zeroed for level k+2
     for (long long i = gt; i < prevN; i += nthreads) {
       const long long at = prev_base + rkp[i];
-      rkp[i] = 0;
+      const_cast<unsigned*>(rkp)[i] = 0;
 #pragma unroll
       for (int w = 0; w < W; w++) fam[at * W + w] = prv[i * 2 * W + w];
     }
@@ -537,6 +658,7 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
     prevN = k <= n ? N : 0;
     base += N;
     grid.sync();
+    k++;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) ls[n + 1] = base;
 }
@@ -562,12 +684,25 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
   DevBuf<long long> ctr, ls;
   static int num_sms = 0;
   if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  // narrow levels (<= ncap members and <= work_cap candidate checks) run in
+  // one block with the level in shared memory (enum_narrow_run)
+  const int ncap = (int)std::min<size_t>(96, (40u << 10) / (2 * 2 * W * sizeof(u64)));
+  const size_t nsm = (size_t)2 * ncap * 2 * W * sizeof(u64);
+  long long work_cap = 1024;  // chain-like levels (DenseNet: 2.1 -> 1.2 ms); C5 keeps the grid walk
+  if (const char* e = getenv("REMAT_ENUM_NARROW_WORK"))  // tuning / test hook (0: off)
+    work_cap = atoll(e);
+  static bool attr = false;
+  if (!attr) {
+    RM_CUDA(cudaFuncSetAttribute(k_enum_all<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)nsm));
+    attr = true;
+  }
   int bps = 0;
-  RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_enum_all<W>, 256, 0));
+  RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_enum_all<W>, 256, nsm));
   if (bps < 1) return fail(REMAT_ERR_CUDA, "enumeration kernel cannot be resident");
   // one block per SM keeps the per-level grid barrier cheap
   const int nblk = num_sms;
-  if ((rc = ctr.ensure(n + 2)) < 0 || (rc = ls.ensure(n + 2)) < 0 || (rc = status.ensure(1)) < 0)
+  if ((rc = ctr.ensure(n + 2)) < 0 || (rc = ls.ensure(n + 2)) < 0 || (rc = status.ensure(2)) < 0)
     return rc;
   while (true) {
     const long long ucap = (long long)std::min<long double>((long double)fcap, binom + 1);
@@ -577,7 +712,7 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
     RM_CUDA(cudaMemsetAsync(U.p, 0, sizeof(u64) * 2 * W, s));  // the empty set, no maximal elements
     RM_CUDA(cudaMemsetAsync(rank.p, 0, sizeof(unsigned) * 3 * ucap, s));
     RM_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(long long) * (n + 2), s));
-    RM_CUDA(cudaMemsetAsync(status.p, 0, sizeof(int), s));
+    RM_CUDA(cudaMemsetAsync(status.p, 0, 2 * sizeof(int), s));
     const long long one = 1;
     RM_CUDA(cudaMemcpyAsync(ctr.p, &one, sizeof one, cudaMemcpyHostToDevice, s));
     const u64* preds = g->preds.p;
@@ -586,11 +721,11 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
     unsigned* a2 = rank.p;
     long long *a3 = ctr.p, *a4 = ls.p;
     int* a5 = status.p;
-    int nn = n;
-    long long cp = cap;
-    void* args[] = {(void*)&preds, &nn, &cp, &fc, &a0, &a1, &uc, &a2, &a3, &a4, &a5};
+    int nn = n, nc = ncap;
+    long long cp = cap, wc = work_cap;
+    void* args[] = {(void*)&preds, &nn, &cp, &fc, &a0, &a1, &uc, &a2, &a3, &a4, &a5, &nc, &wc};
     RM_CUDA(cudaLaunchCooperativeKernel((const void*)k_enum_all<W>, dim3(nblk), dim3(256), args,
-                                        0, s));
+                                        nsm, s));
     RM_LAUNCHED();
     int st = 0;
     level_start.assign(n + 2, 0);
