@@ -14,9 +14,13 @@ s.close()
 g = named_graph("random-dag", depth=64, edge_prob=0.4, seed=0)
 print(dp_plan(PlanRequest(g, 2 * g.total_memory, "full")).objective_value)
 print(loopback_plans(g, [100], 3)[0].objective_value)
+g = named_graph("resnet50")  # chain-like pruned family: one predecessor per warp, split tiles
+print(dp_plan(PlanRequest(g, 6929, "pruned")).objective_value)
+g = named_graph("densenet161")  # chain lattice: single-block enumeration runs
+print(dp_plan(PlanRequest(g, 2 * g.total_memory, "full", "maximize")).objective_value)
 PY
 timeout 1200 compute-sanitizer --tool memcheck --leak-check no python /tmp/san.py > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/memcheck.log
 REMAT_FORCE_WIDE=1 timeout 1200 compute-sanitizer --tool memcheck python /tmp/san.py > gpurun_out/memcheck_wide.log 2>&1; echo "rc=$?" >> gpurun_out/memcheck_wide.log
 timeout 1800 compute-sanitizer --tool racecheck python /tmp/san.py > gpurun_out/racecheck.log 2>&1; echo "racecheck rc=$?" >> gpurun_out/racecheck.log
 timeout 1200 compute-sanitizer --tool synccheck python /tmp/san.py > gpurun_out/synccheck.log 2>&1; echo "synccheck rc=$?" >> gpurun_out/synccheck.log
-tail -3 gpurun_out/memcheck.log gpurun_out/memcheck_wide.log gpurun_out/racecheck.log gpurun_out/synccheck.log
+tail -n 3 gpurun_out/memcheck.log gpurun_out/memcheck_wide.log gpurun_out/racecheck.log gpurun_out/synccheck.log
