@@ -12,4 +12,4 @@ timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/b
 bash tools/gpu_launches.sh
 bash tools/gpu_traffic.sh unet
 bash tools/gpu_prof.sh k_relax_tile 14
-tail -2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; head -c 600 gpurun_out/bench.json; echo
+tail -n 2 gpurun_out/pytest_gpu.log gpurun_out/smoke.log; head -c 600 gpurun_out/bench.json; echo
