@@ -28,6 +28,18 @@ void prepare_pool(int device) {
   }
   done[device] = true;
 }
+int sm_count(int device) {
+  static std::atomic<int> sms[kMaxDevices] = {};
+  const int d = dev_slot(device);
+  int v = sms[d].load();
+  if (!v) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v < 1)
+      v = 148;
+    sms[d].store(v);
+  }
+  return v;
+}
+
 static std::atomic<long long> g_launches{0};
 
 void set_error(int code, const std::string& msg) {

@@ -682,8 +682,7 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
   DevBuf<unsigned> rank;
   DevBuf<int> status;
   DevBuf<long long> ctr, ls;
-  static int num_sms = 0;
-  if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  const int num_sms = sm_count(g->device);
   // narrow levels (<= ncap members and <= work_cap candidate checks) run in
   // one block with the level in shared memory (enum_narrow_run)
   const int ncap = (int)std::min<size_t>(96, (40u << 10) / (2 * 2 * W * sizeof(u64)));
@@ -691,11 +690,11 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
   long long work_cap = 1024;  // chain-like levels (DenseNet: 2.1 -> 1.2 ms); C5 keeps the grid walk
   if (const char* e = getenv("REMAT_ENUM_NARROW_WORK"))  // tuning / test hook (0: off)
     work_cap = atoll(e);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};
+  if (!attr[dev_slot(g->device)]) {
     RM_CUDA(cudaFuncSetAttribute(k_enum_all<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)nsm));
-    attr = true;
+    attr[dev_slot(g->device)] = true;
   }
   int bps = 0;
   RM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_enum_all<W>, 256, nsm));

@@ -76,6 +76,12 @@ struct Status {
   bool ok() const { return code >= 0; }
 };
 
+// Facts and one-time setup CUDA keeps per device (SM count, kernel function
+// attributes) are cached per device id: one process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+inline int dev_slot(int device) { return device >= 0 && device < kMaxDevices ? device : 0; }
+int sm_count(int device);
+
 void set_error(int code, const std::string& msg);
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);

@@ -1083,11 +1083,11 @@ int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int object
       (rc = f->terms.ensure((size_t)nb * (n + 1) * 4)) < 0 ||
       (rc = f->stage_bound.ensure((size_t)nb * (n + 1) * W)) < 0)
     return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  if (!attr_set[dev_slot(g->device)]) {
     RM_CUDA(cudaFuncSetAttribute(relax_tile_kernel<W, NARROW>(),
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-    attr_set = true;
+    attr_set[dev_slot(g->device)] = true;
   }
   f->cur_nb = nb;
   f->cur_objective = objective;
@@ -1144,8 +1144,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   const GraphView gv = g->view();
   const ClassView cv = g->classes();
   const int K = cv.K;
-  static int num_sms = 0;
-  if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  const int num_sms = sm_count(g->device);
   const long long target_ctas = (long long)num_sms * 4;  // resident CTAs at 256 threads
   const long long j0 = f->level_start[lvl];               // predecessors: [0, j0)
   const long long width = hi - lo;
@@ -1230,15 +1229,13 @@ template <int W, bool NARROW>
 int levels_w(remat_family_s* f, const std::vector<int>& lvls) {
   std::vector<TileArgs> tas(lvls.size());
   int maxbytes = 0, rc;
-  static int attr_bytes = -1;
-  if (attr_bytes < 0) {
+  static bool attr[kMaxDevices] = {};
+  if (!attr[dev_slot(f->g->device)]) {
     RM_CUDA(cudaFuncSetAttribute(k_relax_levels<W, NARROW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-    attr_bytes = kSmemLimit;
+    attr[dev_slot(f->g->device)] = true;
   }
-  static int num_sms0 = 0;
-  if (!num_sms0)
-    RM_CUDA(cudaDeviceGetAttribute(&num_sms0, cudaDevAttrMultiProcessorCount, f->g->device));
+  const int num_sms0 = sm_count(f->g->device);
   // size the grid from a first plan, then re-plan every level for one round
   for (int pass = 0; pass < 2; pass++) {
     long long grid = 0;
@@ -1265,8 +1262,7 @@ int levels_w(remat_family_s* f, const std::vector<int>& lvls) {
       if ((rc = level_w<W, NARROW>(f, l, f->level_start[l], f->level_start[l + 1])) < 0) return rc;
     return REMAT_OK;
   }
-  static int num_sms = 0;
-  if (!num_sms) RM_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, f->g->device));
+  const int num_sms = sm_count(f->g->device);
   cudaStream_t s = f->g->stream;
   if ((rc = f->levelargs.ensure(tas.size() * sizeof(TileArgs))) < 0) return rc;
   RM_CUDA(cudaMemcpyAsync(f->levelargs.p, tas.data(), tas.size() * sizeof(TileArgs),
@@ -1306,11 +1302,11 @@ int small_w(remat_family_s* f) {
   int stride = 1;
   for (auto& ta : tas) stride = std::max(stride, ta.tiles);
   for (auto& ta : tas) ta.ctr_stride = stride;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kMaxDevices] = {};
+  if (!attr[dev_slot(f->g->device)]) {
     RM_CUDA(cudaFuncSetAttribute(k_solve_small<W, NARROW>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
-    attr = true;
+    attr[dev_slot(f->g->device)] = true;
   }
   cudaStream_t s = f->g->stream;
   if ((rc = f->levelargs.ensure(tas.size() * sizeof(TileArgs))) < 0) return rc;
