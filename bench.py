@@ -65,7 +65,10 @@ class ClockSampler:
     (between ``start()`` and ``stop()``)."""
 
     def __init__(self, index: int):
-        self.index = index
+        # nvidia-smi counts physical GPUs: map the CUDA ordinal through
+        # CUDA_VISIBLE_DEVICES (indices or UUIDs) when it is set
+        vis = [x.strip() for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
+        self.index = vis[index] if index < len(vis) else index
         self.rows: list[tuple[float, list[str]]] = []
         self.proc = None
         self.t0 = self.t1 = None
