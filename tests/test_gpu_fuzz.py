@@ -67,3 +67,31 @@ def test_fuzz_against_oracle(seed):
             assert b_min == ref_b
             assert_plan_matches(plan, ref, (seed, kind, fam, "bmin"))
             s.close()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fuzz_level_sharding_loopback_against_oracle(seed):
+    """The level-sharded exchange (pack, all-gather, unpack per level) with
+    2..5 replicas on one device, on the fuzz graphs: every field equals the
+    oracle's, both objectives, pruned and full families."""
+    from oracle import oracle as orc
+    from paper_1905_11722_b200.shard import loopback_plans
+
+    rng = random.Random(5000 + seed)
+    done = 0
+    while done < 2:
+        g, kind = _graph(rng)
+        try:
+            orc.family(g, "full", 5_000)
+        except RuntimeError:
+            continue
+        done += 1
+        world = rng.randint(2, 5)
+        top = 2 * g.total_memory
+        budgets = sorted({rng.randint(0, top) for _ in range(3)} | {top})
+        for fam in ("full", "pruned"):
+            for obj in ("minimize", "maximize"):
+                plans = loopback_plans(g, budgets, world, fam, obj, 5_000)
+                for b, plan in zip(budgets, plans):
+                    ref = orc.dp_plan(g, b, fam, obj, cap=5_000)
+                    assert_plan_matches(plan, ref, (seed, kind, world, fam, obj, b))
