@@ -456,14 +456,18 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   // the first chunk of every warp is static (CTA rank within the tile x warps
   // + warp), later ones come from the counter, offset past the static ones
   const long long nstatic = (long long)splits * kWarps;
-  auto next_chunk = [&]() {
+  // (the one-CTA-per-budget solver deals its chunks round-robin: a level's
+  // few chunks are too even to need balancing, and each counter round trip
+  // sits on the level-to-level critical path)
+  auto next_chunk = [&](long long ch) {
+    if constexpr (DUAL) return ch + nstatic;
     if (nstatic >= nch) return nch;  // the static chunks covered the range
     unsigned got = 0;
     if (lane == 0) got = atomicAdd(ctr, 1u);
     return nstatic + (long long)__shfl_sync(kFull, got, 0);
   };
   for (long long ch = (long long)(vbx - tile * splits) * kWarps + warp; ch < nch;
-       ch = next_chunk()) {
+       ch = next_chunk(ch)) {
     worked = true;
     // lane = predecessor i: its set and scalars in one round of loads
     const long long i = ch * cw + lane;
