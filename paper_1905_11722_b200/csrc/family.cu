@@ -668,11 +668,14 @@ static int enumerate_full(remat_graph_s* g, long long cap, DevBuf<u64>& fam,
                           std::vector<long long>& level_start) {
   cudaStream_t s = g->stream;
   const int n = g->n;
-  // Buffers start at min(cap, 4 M members) and grow 4x (rerun) only when the
+  // Buffers start at min(cap, 256 K members) and grow 4x (rerun) only when the
   // lattice outgrows them below the cap; the three level buffers hold one
   // level each, and no level is wider than C(n, n/2) nor than the family.
   const long long capn = std::max<long long>(cap, n + 1);
-  long long fcap = std::min<long long>(capn, 4LL << 20);
+  // (256 K members: every named config fits the first pass; buffers sized for
+  // millions of members made every small family build churn ~1 GB of pool
+  // memory against the solver's own tables)
+  long long fcap = std::min<long long>(capn, 256LL << 10);
   if (const char* e = getenv("REMAT_ENUM_INIT_CAP"))  // test hook for the grow path
     fcap = std::min<long long>(capn, std::max<long long>(n + 1, atoll(e)));
   long double binom = 1;
