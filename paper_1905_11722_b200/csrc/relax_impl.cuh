@@ -35,10 +35,11 @@ struct __align__(16) PairQW {
   int pad;
 };
 
-// A live predecessor of a warp's chunk: its entries start at table index
-// base + (item offset), its budget-feasible pairs are wq[q0, q1).
+// A live predecessor of a warp's chunk: its entry for item offset e is at
+// ptr + e (a ready address: no index arithmetic per item), its budget-feasible
+// pairs are wq[q0, q1).
 struct __align__(16) PredRec {
-  long long base;
+  const void* ptr;  // address of the predecessor's entry for item offset 0
   int q0, q1;
 };
 
@@ -601,7 +602,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     const int start = c > 0 ? iincl - c : INT_MAX;
     if (c > 0) {
       PredRec rc;
-      rc.base = fbase + foffi - (iincl - c);
+      rc.ptr = fe + (fbase + foffi - (iincl - c));
       rc.q0 = lane * TJ;
       rc.q1 = lane * TJ + pc;
       wrec[__popc(has & lt)] = rc;
@@ -635,7 +636,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         v = lane < tot;
         if (v) {
           rec = wrec[k];
-          Traits<NARROW>::template load<COH>(fe + (rec.base + lane), t, m);
+          Traits<NARROW>::template load<COH>(static_cast<const E*>(rec.ptr) + lane, t, m);
         }
       }
       for (int r = 0; r < tot; r += 32) {
@@ -648,7 +649,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           vn = r + 32 + lane < tot;
           if (vn) {
             recn = wrec[kn];
-            Traits<NARROW>::template load<COH>(fe + (recn.base + r + 32 + lane), tn, mn);
+            Traits<NARROW>::template load<COH>(static_cast<const E*>(recn.ptr) + (r + 32 + lane), tn, mn);
           }
         }
         if (v) {
@@ -703,11 +704,11 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         x1.v = e0 + 1 < tot;
         if (x0.v) {
           x0.rec = wrec[k0];
-          Traits<NARROW>::template load<COH>(fe + (x0.rec.base + e0), x0.t, x0.m);
+          Traits<NARROW>::template load<COH>(static_cast<const E*>(x0.rec.ptr) + e0, x0.t, x0.m);
         }
         if (x1.v) {
           x1.rec = wrec[k1];
-          Traits<NARROW>::template load<COH>(fe + (x1.rec.base + e0 + 1), x1.t, x1.m);
+          Traits<NARROW>::template load<COH>(static_cast<const E*>(x1.rec.ptr) + (e0 + 1), x1.t, x1.m);
         }
       };
       auto relax = [&](const Item& x) {
