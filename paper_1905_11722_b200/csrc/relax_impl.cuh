@@ -36,11 +36,11 @@ struct __align__(16) PairQW {
 };
 
 // A live predecessor of a warp's chunk: its entry for item offset e is at
-// ptr + e (a ready address: no index arithmetic per item), its budget-feasible
-// pairs are wq[q0, q1).
+// ptr + e, its budget-feasible pairs are the records at shared addresses
+// [a0, a1) (ready addresses: no index arithmetic per item).
 struct __align__(16) PredRec {
   const void* ptr;  // address of the predecessor's entry for item offset 0
-  int q0, q1;
+  unsigned a0, a1;  // shared-window byte addresses of wq[q0], wq[q1]
 };
 
 template <bool NARROW>
@@ -173,26 +173,39 @@ __device__ __forceinline__ void key_min(u64* p, u64 key, bool smem) {
 __device__ __forceinline__ void red_smem(unsigned a, unsigned key, bool ok) {
   asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(a), "r"(ok ? key : 0xffffffffu));
 }
-// All pairs [qp, qe) of one item (entry t, m; mk = m << IB, t4 = 4t), four
+// All pairs [a, e) (shared addresses of records) of one item (entry t, m;
+// mk = m << IB, t4 = 4t), four
 // records per step so four LDS.128 are in flight (U-Net c=8: 4 -> 2 per step
 // costs 0.6 %, 1 per step 4 %).
-__device__ __forceinline__ void red_pairs(const PairQN* qp, const PairQN* qe, unsigned t4,
-                                          unsigned mk, unsigned m) {
-  for (; qp + 3 < qe; qp += 4) {
-    const PairQN p0 = Traits<true>::lds(qp), p1 = Traits<true>::lds(qp + 1);
-    const PairQN p2 = Traits<true>::lds(qp + 2), p3 = Traits<true>::lds(qp + 3);
+__device__ __forceinline__ PairQN lds_pair(unsigned a) {  // one LDS.128
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a));
+  PairQN q;
+  q.base = (int)v.x;
+  q.cap = v.y;
+  q.kb = v.z;
+  q.dtr = (int)v.w;
+  return q;
+}
+__device__ __forceinline__ void red_pairs(unsigned a, const unsigned e, unsigned t4, unsigned mk,
+                                          unsigned m) {
+  for (; a + 48 < e; a += 64) {
+    const PairQN p0 = lds_pair(a), p1 = lds_pair(a + 16);
+    const PairQN p2 = lds_pair(a + 32), p3 = lds_pair(a + 48);
     red_smem(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap);
     red_smem(t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
     red_smem(t4 + (unsigned)p2.base, mk + p2.kb, m <= p2.cap);
     red_smem(t4 + (unsigned)p3.base, mk + p3.kb, m <= p3.cap);
   }
-  for (; qp + 1 < qe; qp += 2) {
-    const PairQN p0 = Traits<true>::lds(qp), p1 = Traits<true>::lds(qp + 1);
+  for (; a + 16 < e; a += 32) {
+    const PairQN p0 = lds_pair(a), p1 = lds_pair(a + 16);
     red_smem(t4 + (unsigned)p0.base, mk + p0.kb, m <= p0.cap);
     red_smem(t4 + (unsigned)p1.base, mk + p1.kb, m <= p1.cap);
   }
-  if (qp < qe) {
-    const PairQN p = Traits<true>::lds(qp);
+  if (a < e) {
+    const PairQN p = lds_pair(a);
     red_smem(t4 + (unsigned)p.base, mk + p.kb, m <= p.cap);
   }
 }
@@ -388,6 +401,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
   unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
   Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * 32 * TJ;  // feasible pairs of a chunk
+  const unsigned wq_sa = (unsigned)__cvta_generic_to_shared(wq);
   PredRec* wrec = reinterpret_cast<PredRec*>(sm + ta.off_qs) + warp * 32;  // live predecessors
   int* wpc = reinterpret_cast<int*>(sm + ta.off_qs + kWarps * 32 * 16) + warp * 32;
   Key* grow_t = ta.grow ? reinterpret_cast<Key*>(ta.grow) +
@@ -603,8 +617,8 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     if (c > 0) {
       PredRec rc;
       rc.ptr = fe + (fbase + foffi - (iincl - c));
-      rc.q0 = lane * TJ;
-      rc.q1 = lane * TJ + pc;
+      rc.a0 = wq_sa + (unsigned)(lane * TJ * sizeof(Q));
+      rc.a1 = rc.a0 + (unsigned)(pc * sizeof(Q));
       wrec[__popc(has & lt)] = rc;
     }
     __syncwarp();
@@ -655,17 +669,19 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         if (v) {
           const Key mk = (Key)m << IB;
           const unsigned t4 = 4u * t;
-          const Q* qe = wq + rec.q1;
-          const Q* qp = wq + rec.q0;
+          bool done = false;
           if constexpr (NARROW) {
             if (smem) {
-              red_pairs(qp, qe, t4, mk, m);
-              qp = qe;
+              red_pairs(rec.a0, rec.a1, t4, mk, m);
+              done = true;
             }
           }
-          for (; qp < qe; ++qp) {
-            const Q p = Traits<NARROW>::lds(qp);
-            if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
+          if (!done) {
+            const Q* qe = wq + (rec.a1 - wq_sa) / sizeof(Q);
+            for (const Q* qp = wq + (rec.a0 - wq_sa) / sizeof(Q); qp < qe; ++qp) {
+              const Q p = Traits<NARROW>::lds(qp);
+              if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
+            }
           }
         }
         rec = recn;
@@ -716,15 +732,14 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         const MT m = x.m;
         const Key mk = (Key)m << IB;
         const unsigned t4 = 4u * t;
-        const Q* qe = wq + x.rec.q1;
-        const Q* qp = wq + x.rec.q0;
         if constexpr (NARROW) {
           if (smem) {
-            red_pairs(qp, qe, t4, mk, m);
+            red_pairs(x.rec.a0, x.rec.a1, t4, mk, m);
             return;
           }
         }
-        for (; qp < qe; ++qp) {
+        const Q* qe = wq + (x.rec.a1 - wq_sa) / sizeof(Q);
+        for (const Q* qp = wq + (x.rec.a0 - wq_sa) / sizeof(Q); qp < qe; ++qp) {
           const Q p = Traits<NARROW>::lds(qp);
           if (m <= p.cap) key_min(rw + (t + p.dtr), mk + (Key)p.kb, smem);
         }
