@@ -42,6 +42,17 @@ struct __align__(16) PredRec {
   const void* ptr;  // address of the predecessor's entry for item offset 0
   unsigned a0, a1;  // shared-window byte addresses of wq[q0], wq[q1]
 };
+__device__ __forceinline__ PredRec ld_rec(const PredRec* p) {  // one LDS.128
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"((unsigned)__cvta_generic_to_shared(p)));
+  PredRec r;
+  r.ptr = reinterpret_cast<const void*>(((unsigned long long)v.y << 32) | v.x);
+  r.a0 = v.z;
+  r.a1 = v.w;
+  return r;
+}
 
 template <bool NARROW>
 struct Traits;
@@ -649,7 +660,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         const int k = map_step(0);
         v = lane < tot;
         if (v) {
-          rec = wrec[k];
+          rec = ld_rec(wrec + k);
           Traits<NARROW>::template load<COH>(static_cast<const E*>(rec.ptr) + lane, t, m);
         }
       }
@@ -662,7 +673,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           const int kn = map_step(r + 32);
           vn = r + 32 + lane < tot;
           if (vn) {
-            recn = wrec[kn];
+            recn = ld_rec(wrec + kn);
             Traits<NARROW>::template load<COH>(static_cast<const E*>(recn.ptr) + (r + 32 + lane), tn, mn);
           }
         }
