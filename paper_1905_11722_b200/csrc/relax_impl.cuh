@@ -1186,7 +1186,9 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   const long long nch = (j0 + 31) / 32;
   // fewer targets per tile where the level is too small to give every
   // resident warp a couple of (tile, chunk) tasks
-  const long long want = (long long)num_sms * 64;
+  // (32 tasks per SM and 3 resident-CTA rounds of splits: swept on the B200
+  // against 16-64 and 1-8; U-Net relax -2.2 %, C5 p=0.3 -3.6 % vs 64 / 2)
+  const long long want = (long long)num_sms * 32;
   while (!single_cta && TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
   const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
   ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
@@ -1207,7 +1209,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   const long long nchw = (j0 + cw - 1) / cw;
   // split the predecessor scan across CTAs when the level alone cannot fill
   // the GPU (narrow levels near ∅ and V; SURVEY §7 hard part 5)
-  long long splits = (2 * target_ctas + tiles * nb - 1) / (tiles * nb);
+  long long splits = (3 * target_ctas + tiles * nb - 1) / (tiles * nb);
   if (max_vctas > 0) splits = max_vctas / (tiles * nb);  // persistent: one round per block
   if (single_cta) splits = 1;
   // (rounded up: every chunk of a narrow level is some warp's static first one)
