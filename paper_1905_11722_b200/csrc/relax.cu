@@ -52,7 +52,7 @@ namespace remat {
 
 // levels with at most this many (target, predecessor) subset tests are batched
 // into one cooperative launch (their work is a fraction of one GPU wave)
-static constexpr long long kSmallLevelTests = 4LL << 20;
+static constexpr long long kSmallLevelTests = 2LL << 20;  // swept 1-16 M on the B200
 static constexpr long long kSmallLevelPreds = 32LL << 10;
 // families up to this size may be solved by one CTA per budget (k_solve_small)
 static constexpr long long kSmallFamily = 1100;
