@@ -134,11 +134,18 @@ class Solver:
             raise ValueError(f"objective must be one of {OBJECTIVES}, got {objective!r}")
         if probes_per_round is None:
             # small families: maximize rounds run one budget per CTA (144 probes
-            # cost what one does); minimize rounds spread every probe over CTAs
+            # cost what one does); minimize rounds spread every probe over CTAs.
+            # Larger families fill the GPU with fewer probes: a round of k
+            # probes costs ~k solves, so the search narrows to binary as the
+            # family grows (measured on the B200: tools/probe_sweep2.py)
             if self.dev.size <= SMALL_FAMILY:
                 probes_per_round = 144 if objective == "maximize" else 32
+            elif self.dev.size <= 15_000:
+                probes_per_round = 4
+            elif self.dev.size <= 40_000:
+                probes_per_round = 2
             else:
-                probes_per_round = 8
+                probes_per_round = 1
         t0 = time.perf_counter()
         bmin, raw, search = self.dev.min_feasible_budget(objective, probes_per_round)
         wall = time.perf_counter() - t0
