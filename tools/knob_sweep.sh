@@ -1,5 +1,8 @@
 #!/bin/bash
-# one pass of relax_probe (+ the C4 sweep) per library variant / env knob
+# one pass of relax_probe (+ the C4 sweep) per library variant
+# (paper_1905_11722_b200/libremat_b200*.so, built with make EXTRA=-D... OUT=...).
+# The planner constants it was used to sweep (tasks per SM, split rounds,
+# small-level threshold) are now fixed in relax_impl.cuh / relax.cu.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 probe() { timeout 300 python tools/relax_probe.py --big; timeout 300 python - <<'PY'
@@ -15,5 +18,3 @@ s.plans(b); t0 = time.perf_counter(); s.plans(b); print("C4 full sweep ms", roun
 PY
 }
 for lib in paper_1905_11722_b200/libremat_b200*.so; do echo "== $lib"; REMAT_B200_LIB=$PWD/$lib probe; done
-for v in 32 128; do echo "== REMAT_WANT_MUL=$v"; REMAT_WANT_MUL=$v probe; done
-for v in 1 4; do echo "== REMAT_SPLIT_MUL=$v"; REMAT_SPLIT_MUL=$v probe; done
