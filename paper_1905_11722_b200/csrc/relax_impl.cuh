@@ -1190,8 +1190,21 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   // against 16-64 and 1-8; U-Net relax -2.2 %, C5 p=0.3 -3.6 % vs 64 / 2)
   const long long want = (long long)num_sms * 32;
   while (!single_cta && TJ > 1 && ((width + TJ - 1) / TJ) * nch * nb < want) TJ = (TJ + 1) / 2;
-  const bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
+  bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
   ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
+  // fewer targets per tile where the shared-memory tile would cost a resident
+  // CTA: the register-bound occupancy (4 CTAs/SM at 64 registers, 3 for the
+  // wide-bitset kernel) is worth more than two more rows (PSPNet full sweep,
+  // rows of 1.4 k slots: 8 -> 6 targets keeps 3 CTAs/SM, -9 %)
+  if (!single_cta) {
+    const int occ = W >= 4 ? 3 : 4;
+    const int per_cta = (228 << 10) / occ - (1 << 10);
+    while (TJ > 1 && ta.bytes > per_cta) {
+      --TJ;
+      cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
+      ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
+    }
+  }
   if (ta.bytes > kSmemLimit) ta = tile_layout<W, NARROW>(TJ, R, K, false, cls);
   const long long tiles = (width + TJ - 1) / TJ;
   // narrower predecessor chunks where even one target per tile leaves the GPU
