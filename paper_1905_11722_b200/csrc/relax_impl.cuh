@@ -16,6 +16,9 @@ namespace remat {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+// resident CTAs of the wide-bitset relaxation kernel (register cap 64; a
+// 16-byte spill at W = 9; 3 CTAs at 80 registers measured 1 % slower)
+constexpr int kTile3MinBlocks = 4;
 constexpr int kMaxTJ = 8;    // targets per tile (one comparable bit each, <= 32)
 constexpr int kDenseLanes = 16;  // lanes with a pair for lane = predecessor constants
 constexpr int kSmallF = 4;       // frontier entries kept in registers (small-frontier path)
@@ -860,9 +863,9 @@ __global__ void __launch_bounds__(kThreads)
   relax_body<W, NARROW, false>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
 }
 
-// wide bitsets (W >= 4) keep three CTAs per SM resident (<= 80 registers)
+// wide bitsets (W >= 4): register cap for kTile3MinBlocks resident CTAs per SM
 template <int W, bool NARROW>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, kTile3MinBlocks)
     k_relax_tile3(FamilyView fv, GraphView g, ClassView cv, DpView dp, TileArgs ta) {
   extern __shared__ __align__(16) unsigned char sm[];
   relax_body<W, NARROW, false>(fv, g, cv, dp, ta, blockIdx.x, blockIdx.y, gridDim.y, sm);
@@ -1193,11 +1196,11 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   bool cls = cv.enabled && (long long)TJ * K * W * 8 <= 16 * 1024;
   ta = tile_layout<W, NARROW>(TJ, R, K, true, cls);
   // fewer targets per tile where the shared-memory tile would cost a resident
-  // CTA: the register-bound occupancy (4 CTAs/SM at 64 registers, 3 for the
-  // wide-bitset kernel) is worth more than two more rows (PSPNet full sweep,
-  // rows of 1.4 k slots: 8 -> 6 targets keeps 3 CTAs/SM, -9 %)
+  // CTA: the register-bound occupancy (4 CTAs/SM at 64 registers) is worth
+  // more than two more rows (PSPNet full sweep, rows of 1.4 k slots: 8 -> 6
+  // targets kept a third CTA per SM resident, -9 %)
   if (!single_cta) {
-    const int occ = W >= 4 ? 3 : 4;
+    const int occ = W >= 4 ? kTile3MinBlocks : 4;
     const int per_cta = (228 << 10) / occ - (1 << 10);
     while (TJ > 1 && ta.bytes > per_cta) {
       --TJ;
