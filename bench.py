@@ -1,24 +1,35 @@
-"""Benchmark: exact-DP transitions/s on the C2 U-Net config (BASELINE.json
-configs[1]) — one step = one complete exact ``dp_plan`` (full lower-set
-lattice, minimize, B = 2·M(V): every transition feasible, the max-work budget)
-from the graph to the plan's figures.
+"""Benchmark: exact-DP transitions/s, one B200 (or N under torchrun).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--skip-len C] [--workload unet|random-dag]
+                  [--skip-len C] [--no-configs] [--no-cpu]
 
-Prints ONE JSON line (rank 0).  Under torchrun (N > 1) every rank solves the
-same graph at its own budget of a sweep (budget sharding, weak scaling, no
-data-path collective); the barrier + max-over-ranks timing use
-torch.distributed.
+Headline workload (BASELINE.json configs[1]): exact DP on the op-level U-Net
+with skip branch 8 (n=81, F=54,946 lower sets, X=9.72·10⁹ transitions at
+B = 2·M(V), the max-work budget).  One step = one complete exact solve: family
+build + precompute + relaxation + reconstruction + figures.
 
-``value``   device time (CUDA events on the solver's stream) of family build +
-            precompute + relaxation + reconstruction + figures, graph already
-            resident in HBM; L2 flushed (256 MiB write) between steps.
-``e2e``     the public API ``dp_plan(PlanRequest(...))`` with the graph in host
-            memory: H2D upload, solve, D2H of the plan, host wall clock.
-``--impl reference`` times the CPU restatement of the reference solver
-(oracle/, "port": the reference is pure Python and cannot travel to the GPU
-box) on all host cores for the same workload.
+``value``   device time (CUDA events on the solver's stream), graph resident in
+            HBM, L2 flushed (256 MiB write) between steps.  N=1: one GPU.
+            N>1 (torchrun): the SAME solve with every wavefront level's targets
+            sharded over the ranks and one NCCL all-gather per level (strong
+            scaling), max over ranks.
+``e2e``     the public API with the graph in host memory (``dp_plan`` at N=1,
+            ``LevelShardedSolver.plan`` at N>1): upload, solve, plan back.
+``roofline`` the binding roof of the relaxation (essential-work floor on the
+            pipe that bounds it, from the per-SM pipe peaks measured by
+            tools/micro/pipes.cu, ``profiles/pipes.json``); the HBM byte model
+            of SURVEY §8(d) rides along as ``roofline.hbm``.
+``configs`` every other BASELINE config driver-timed in the same run, each
+            checked against its committed golden fixture (tests/golden/*.json:
+            reference outputs, or the pinned oracle's where the Python
+            reference cannot finish): C5 random-dag n=516 at p=0.2 (the
+            north-star largest graph) / 0.3 / 0.4, C1 ResNet-50, the C2 B_min
+            search, C3 DenseNet-161 memory-centric, C4 PSPNet 64-budget sweeps
+            (budget-sharded over the ranks at N>1).
+``--impl reference`` the reference arm: the CPU restatement of the reference
+            solver (oracle/remat_oracle.c, "port", all host threads) on the
+            headline workload, W warm-up + K timed solves, plus the Python
+            reference itself (oracle/_ref, 1 core) on a bounded sample.
 """
 
 from __future__ import annotations
@@ -37,26 +48,38 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 HBM_FALLBACK_GBS = 6650.0
+METRIC = "exact-DP transitions/s (end-to-end solve)"
+GOLDEN = ROOT / "tests" / "golden"
 
+
+# ----------------------------------------------------------------------------
+# peaks, workload, clocks
+# ----------------------------------------------------------------------------
 
 def peaks() -> dict:
+    out = {"hbm_gbs": HBM_FALLBACK_GBS, "hbm_source": "fallback (B200_PROFILING.md)"}
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        return {"hbm_gbs": d["hbm_gbs"], "source": "measured"}
-    return {"hbm_gbs": HBM_FALLBACK_GBS, "source": "fallback"}
+        out.update(hbm_gbs=json.loads(p.read_text())["hbm_gbs"],
+                   hbm_source="MEASURED_PEAKS.json")
+    pipes = ROOT / "profiles" / "pipes.json"
+    out["pipes"] = json.loads(pipes.read_text()) if pipes.exists() else None
+    return out
 
 
-def workload(args):
+def headline(args):
     from paper_1905_11722_b200 import named_graph
 
-    if args.workload == "unet":
-        g = named_graph("unet", skip_len=args.skip_len)
-        name = f"C2 op-level U-Net skip_len={args.skip_len}, exact DP (full lattice), minimize"
-    else:
-        g = named_graph("random-dag", depth=516, edge_prob=args.edge_prob, seed=0)
-        name = f"C5 random-dag n=516 p={args.edge_prob}, exact DP (full lattice), minimize"
-    return g, name
+    g = named_graph("unet", skip_len=args.skip_len)
+    name = f"C2 op-level U-Net skip_len={args.skip_len}, exact DP (full lattice), minimize"
+    return g, name, 2 * g.total_memory
+
+
+def config_of(name, g, budget, F, X, P, E) -> dict:
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": name, "n": g.n, "family_size": F, "budget": budget,
+            "transitions_per_step": X, "comparable_pairs": P, "table_entries": E,
+            "l2": "flushed (256 MiB write) between device-timed steps"}
 
 
 class ClockSampler:
@@ -65,8 +88,6 @@ class ClockSampler:
     (between ``start()`` and ``stop()``)."""
 
     def __init__(self, index: int):
-        # nvidia-smi counts physical GPUs: map the CUDA ordinal through
-        # CUDA_VISIBLE_DEVICES (indices or UUIDs) when it is set
         vis = [x.strip() for x in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if x.strip()]
         self.index = vis[index] if index < len(vis) else index
         self.rows: list[tuple[float, list[str]]] = []
@@ -123,31 +144,72 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------
+# rooflines
+# ----------------------------------------------------------------------------
+
 def q_alg_relax(n: int, X: int, P: int, E: int) -> int:
-    """Algorithmic bytes of the relaxation: each transition reads
-    its source entry once (12 B), each comparable pair the predecessor bitset +
-    M(L_i), T(L_i) once (16·W+16 B, W = ⌈n/128⌉), each table entry is written
-    with its parent (16 B)."""
+    """SURVEY §8(d) algorithmic bytes of the relaxation: 12 B per transition
+    (source entry), 16·W+16 B per comparable pair (predecessor bitset +
+    M(L_i), T(L_i); W = ⌈n/128⌉), 16 B per table entry written."""
     W = (n + 127) // 128
     return 12 * X + (16 * W + 16) * P + 16 * E
 
 
-def family_bytes(n: int, F: int) -> int:
-    W = (n + 127) // 128
-    return (32 * W + 48) * F
+def relax_roofline(n, X, P, E, relax_s, launches, pk, traffic=None) -> dict:
+    """Essential-work floor of the relaxation on the pipe that binds it.
 
+    * every transition (candidate) is at least one shared-memory RED.MIN on
+      its target cell → floor X / (shared-RED lane-op peak);
+    * every comparable pair is at least a W₆₄-word subset test and two
+      W₆₄-word class popcounts → floor 3·W₆₄·P / (int32 lane-op peak).
+
+    The larger floor is the binding roof; ``achieved`` is that pipe's
+    essential work ÷ the measured relaxation time, ``frac`` = floor ÷ time.
+    Peaks: tools/micro/pipes.cu on the B200 (``profiles/pipes.json``)."""
+    pipes = pk["pipes"]
+    w64 = (n + 63) // 64
+    hbm_bytes = q_alg_relax(n, X, P, E)
+    hbm = {"achieved_gbs": hbm_bytes / relax_s / 1e9, "peak_gbs": pk["hbm_gbs"],
+           "frac": hbm_bytes / relax_s / 1e9 / pk["hbm_gbs"], "bytes_per_solve": hbm_bytes,
+           "peak_source": pk["hbm_source"],
+           "note": "SURVEY 8(d) byte model; the table is L2-resident, so HBM does not bind"}
+    if not pipes:
+        return {"bound": "hbm", "achieved": hbm["achieved_gbs"], "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": hbm["frac"], "traffic": traffic,
+                "peak_source": pk["hbm_source"]}
+    red = pipes["red_shared_per_s"]            # lane REDs / s
+    ints = pipes["int32_ops_per_s"]            # lane int32 ops / s
+    red_work, int_work = X, 3 * w64 * P
+    if red_work / red >= int_work / ints:
+        bound, work, peak = "shared-atomic (RED.MIN pipe)", red_work, red
+        what = "transitions (one RED.MIN each)"
+    else:
+        bound, work, peak = "int32 issue", int_work, ints
+        what = f"pair lane-ops (3·W64·P, W64={w64})"
+    achieved = work / relax_s
+    return {"bound": bound, "kernel": "k_relax_tile / k_relax_levels",
+            "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "G lane-ops/s",
+            "frac": achieved / peak, "traffic": traffic, "work": what,
+            "floor_ms": 1e3 * work / peak, "relax_ms": 1e3 * relax_s,
+            "launches_per_solve": launches,
+            "peak_source": "profiles/pipes.json (tools/micro/pipes.cu, measured on the B200)",
+            "hbm": hbm}
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------
 
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 or (args.parallel == "levels" and args.impl == "ours"):
+    if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        os.environ.setdefault("RANK", str(rank))
-        os.environ.setdefault("WORLD_SIZE", str(world))
         backend = "nccl" if args.impl == "ours" else "gloo"
         if backend == "nccl":
             import torch
@@ -176,19 +238,54 @@ def allmax(world, x: float) -> float:
     return float(t.item())
 
 
-def allsum(world, x: int) -> int:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
+# ----------------------------------------------------------------------------
+# golden parity (committed fixtures; bench never runs the oracle for parity)
+# ----------------------------------------------------------------------------
 
-    t = torch.tensor([x], dtype=torch.int64,
-                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return int(t.item())
+def _golden(fname: str):
+    p = GOLDEN / fname
+    return json.loads(p.read_text())["data"] if p.exists() else []
 
 
-def cpu_port(g, budget: int, threads: int) -> tuple[float, dict]:
+def golden_run(fname, name, kw_match, kind, pred=lambda r: True):
+    for rec in _golden(fname):
+        if rec["name"] != name or any(rec["kw"].get(k) != v for k, v in kw_match.items()):
+            continue
+        for r in rec["runs"]:
+            if r["kind"] == kind and pred(r):
+                return r
+    return None
+
+
+def parity(plan, ref) -> str:
+    """'bit-exact' when every PlanResult field matches the golden record."""
+    if ref is None:
+        return "no golden"
+    keys = ("states_visited", "table_entries", "transitions", "dominated_skipped")
+    got = {k: getattr(plan.stats, k) for k in keys}
+    diffs = []
+    if plan.feasible != ref["feasible"]:
+        diffs.append("feasible")
+    if got != {k: ref["stats"][k] for k in keys}:
+        diffs.append("stats")
+    if plan.feasible and ref["feasible"]:
+        if plan.objective_value != ref["objective_value"]:
+            diffs.append("objective")
+        if [format(m, "x") for m in plan.sequence.chain] != [
+                x if isinstance(x, str) else format(x, "x") for x in ref["chain"]]:
+            diffs.append("chain")
+        ev = plan.evaluation
+        if (list(ev.per_stage_memory), ev.peak_memory, ev.cached_total) != (
+                list(ref["per_stage_memory"]), ref["peak_memory"], ref["cached_total"]):
+            diffs.append("figures")
+    return "bit-exact" if not diffs else "MISMATCH: " + ",".join(diffs)
+
+
+# ----------------------------------------------------------------------------
+# the reference arm
+# ----------------------------------------------------------------------------
+
+def cpu_port(g, budget: int, threads: int):
     from oracle import oracle as orc
 
     t0 = time.perf_counter()
@@ -196,44 +293,299 @@ def cpu_port(g, budget: int, threads: int) -> tuple[float, dict]:
     return time.perf_counter() - t0, r
 
 
+def python_reference_sample() -> dict | None:
+    """The Python reference itself (oracle/_ref: ``pip install --target`` of
+    /root/reference, built by oracle/Makefile) on one core, on a bounded sample
+    of the headline's workload family: exact ``dp_plan`` of the U-Net with skip
+    branch 2 at 2·M(V) (its relaxation rate is flat in the skip length,
+    ≈1.3·10⁶ transitions/s for c=2 and c=3)."""
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "remat" / "__init__.py").exists():
+        return None
+    code = (
+        "import sys,time,json,os\n"
+        f"sys.path.insert(0,{str(ref)!r})\n"
+        "os.sched_setaffinity(0,{sorted(os.sched_getaffinity(0))[0]})\n"
+        "from remat.graph import graph_from_document\n"
+        "from remat.planner import dp_plan, PlanRequest\n"
+        f"sys.path.insert(0,{str(ROOT)!r})\n"
+        "from paper_1905_11722_b200.benchmarks import unet_document\n"
+        "g=graph_from_document(unet_document(2))\n"
+        "t0=time.perf_counter(); r=dp_plan(PlanRequest(g,2*g.total_memory,'full'))\n"
+        "dt=time.perf_counter()-t0\n"
+        "print(json.dumps({'s':dt,'X':r.stats.transitions,'t':r.objective_value}))\n")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                             timeout=300, env={**os.environ, "PYTHONDONTWRITEBYTECODE": "1"})
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # report, never fail the bench on the sample
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    return {"value": d["X"] / d["s"], "unit": "transitions/s", "cores": 1, "kind": "reference",
+            "seconds": d["s"],
+            "sample": f"Python reference (oracle/_ref, remat 0.1.0) dp_plan on U-Net skip_len=2, "
+                      f"full family, B=2M(V): X={d['X']} transitions in {d['s']:.2f} s; "
+                      f"the headline U-Net c=8 (X=9.7e9) would take ≈{9.72e9 / (d['X'] / d['s']) / 3600:.1f} h"}
+
+
 def run_reference(args, world, rank):
-    """The reference arm: the CPU port of the reference solver on host cores."""
+    """Reference arm: the CPU port of the reference solver (all host threads)
+    on the headline workload — W warm-up + K timed solves of that exact
+    graph/budget — plus the Python reference on its bounded sample."""
     if rank != 0:
         return
-    g, name = workload(args)
+    g, name, budget = headline(args)
     threads = len(os.sched_getaffinity(0))
-    budget = 2 * g.total_memory
-    from paper_1905_11722_b200 import named_graph
-
-    small = named_graph("unet", skip_len=3)
-    for _ in range(args.warmup):  # warm the library/page cache on a small sample
-        cpu_port(small, 2 * small.total_memory, threads)
-    times, X = [], 0
-    # a bounded sample: at most 3 full solves (~8 s each on 16 host threads)
-    nsolve = max(1, min(args.steps, 3))
-    for _ in range(nsolve):
+    for _ in range(args.warmup):
+        cpu_port(g, budget, threads)
+    times, r = [], None
+    for _ in range(args.steps):
         dt, r = cpu_port(g, budget, threads)
         times.append(dt)
-        X = r["stats"]["transitions"]
     total = sum(times)
-    value = X * nsolve / total
+    X = r["stats"]["transitions"]
+    value = X * args.steps / total
+    pyref = python_reference_sample()
     line = {
-        "impl": "reference",
-        "metric": "exact-DP transitions/s (end-to-end solve)",
+        "impl": "reference", "metric": METRIC,
         "value": value, "unit": "transitions/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / nsolve,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
-        "data": "synthetic",
-        "config": {"workload": name, "n": g.n, "family_size": r["family_size"],
-                   "budget": budget, "transitions_per_step": X},
-        "cpu_baseline": {"value": value, "unit": "transitions/s", "cores": threads,
-                         "kind": "port",
-                         "sample": f"{nsolve} full dp_plan solves of the workload "
-                                   "(oracle/remat_oracle.c, OpenMP)"},
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": config_of(name, g, budget, r["family_size"], X, r.get("pairs_expanded"),
+                            r["stats"]["table_entries"]),
+        "parallelism": f"{threads} host threads (OpenMP)",
+        "cpu_baseline": {"value": value, "unit": "transitions/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} timed full dp_plan solves of the workload after "
+                                   f"{args.warmup} warm-up solves (oracle/remat_oracle.c, OpenMP)",
+                         "python_reference": pyref},
         "e2e": {"value": value, "unit": "transitions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+class DeviceSolve:
+    """One exact solve on the device, timed with CUDA events on the solver's
+    stream (family build + precompute + relax + reconstruction + figures)."""
+
+    def __init__(self, g, local, world, budget):
+        import torch
+
+        from paper_1905_11722_b200._native import DeviceGraph
+
+        self.g, self.world, self.budget, self.local = g, world, budget, local
+        self.dg = DeviceGraph(g, local)
+        self.stream = torch.cuda.ExternalStream(self.dg.stream(), device=local)
+        self.comm = None
+        if world > 1:
+            from paper_1905_11722_b200.shard import communicator
+
+            self.comm = communicator(local)
+
+    def once(self):
+        from paper_1905_11722_b200._native import DeviceFamily
+
+        fam = DeviceFamily(self.dg, "full", 2_000_000)
+        if self.comm is not None:
+            info = fam.solve_level_sharded(self.comm, [self.budget], "minimize")[0][0]
+        else:
+            info = fam.solve([self.budget], "minimize")[0][0]
+        return fam, info
+
+    def timed(self, steps, warmup, flush=None, clocks=None):
+        import torch
+
+        for _ in range(warmup):
+            self.once()[0].close()
+        torch.cuda.synchronize()
+        acc = {"relax_ms": 0.0, "enumerate_ms": 0.0, "precompute_ms": 0.0, "relax_launches": 0}
+        from paper_1905_11722_b200._native import kernel_launches
+
+        dev_ms, last = 0.0, None
+        n0 = kernel_launches()
+        if clocks:
+            clocks.start()
+        for _ in range(steps):
+            if flush is not None:
+                flush.zero_()
+            torch.cuda.synchronize()
+            barrier(self.world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(self.stream):
+                e0.record(self.stream)
+                fam, info = self.once()
+                e1.record(self.stream)
+            torch.cuda.synchronize()
+            barrier(self.world)
+            dev_ms += e0.elapsed_time(e1)
+            t = fam.timings()
+            for k in acc:
+                acc[k] += t[k]
+            last = (info, t, fam.size)
+            fam.close()
+        if clocks:
+            clocks.stop()
+        launches = kernel_launches() - n0
+        info, t, F = last
+        return {"ms": allmax(self.world, dev_ms) / steps, "info": info, "F": F,
+                "launches": launches,
+                "P": t["comparable_pairs"],
+                "phases": {k: v / steps for k, v in acc.items()}}
+
+    def close(self):
+        self.dg.close()
+
+
+def e2e_exact(g, budget, world, reps):
+    """The public API, graph in host memory: dp_plan (N=1) or the
+    level-sharded solver (N>1); mean seconds per call, max over ranks."""
+    from paper_1905_11722_b200 import PlanRequest, dp_plan
+
+    ts, plan = [], None
+    for _ in range(reps):
+        barrier(world)
+        t0 = time.perf_counter()
+        if world > 1:
+            from paper_1905_11722_b200.shard import LevelShardedSolver
+
+            ls = LevelShardedSolver(g, "full")
+            plan = ls.plan(budget)
+            ls.close()
+        else:
+            plan = dp_plan(PlanRequest(g, budget, "full", "minimize"))
+        ts.append(time.perf_counter() - t0)
+    return allmax(world, sum(ts) / len(ts)), plan
+
+
+def exact_config(label, g, budget, world, local, steps, warmup, pk, golden):
+    """A C5-style exact solve: device-timed steps + e2e + golden parity."""
+    ds = DeviceSolve(g, local, world, budget)
+    r = ds.timed(steps, warmup)
+    ds.close()
+    e2e_s, plan = e2e_exact(g, budget, world, max(1, min(steps, 3)))
+    X, E = plan.stats.transitions, plan.stats.table_entries
+    ph = r["phases"]
+    return {"config": label, "call": "dp_plan" if world == 1 else "LevelShardedSolver.plan",
+            "n": g.n, "family_size": r["F"], "budget": budget, "transitions": X,
+            "comparable_pairs": r["P"], "device_ms": r["ms"],
+            "transitions_per_s": X / (r["ms"] / 1e3), "e2e_ms": 1e3 * e2e_s,
+            "e2e_transitions_per_s": X / e2e_s, "phase_ms": ph,
+            "roofline": relax_roofline(g.n, X, r["P"], E, ph["relax_ms"] / 1e3,
+                                       ph["relax_launches"], pk),
+            "parity": parity(plan, golden),
+            "parallelism": f"level-sharded x{world}" if world > 1 else "single GPU",
+            "scaling": "strong" if world > 1 else None}
+
+
+def timed_calls(fn, world, reps):
+    ts, out = [], None
+    for _ in range(reps):
+        barrier(world)
+        t0 = time.perf_counter()
+        out = fn()
+        ts.append(time.perf_counter() - t0)
+    return 1e3 * allmax(world, sum(ts) / len(ts)), out
+
+
+def other_configs(args, world, rank, local, pk) -> list:
+    """Every other BASELINE config, driver-timed in this run, each checked
+    against its committed golden fixture."""
+    from paper_1905_11722_b200 import (
+        PlanRequest, dp_plan, liveness_pass, memory_centric_plan, min_feasible_budget,
+        named_graph, simulate, vanilla_schedule,
+    )
+    from paper_1905_11722_b200.sweep import budget_sweep, sweep_budgets
+
+    reps = max(1, min(args.steps, 5))
+    out = []
+
+    def guard(label, fn):
+        try:
+            out.append(fn())
+        except Exception as exc:  # a failed config is reported, not fatal
+            out.append({"config": label, "error": f"{type(exc).__name__}: {exc}"[:300]})
+
+    # C5: the north-star largest graph (and the reference-checkable sizes)
+    for p, fname in ((0.2, "oracle_large.json"), (0.3, "oracle_large.json"),
+                     (0.4, "named_xslow.json")):
+        g = named_graph("random-dag", depth=516, edge_prob=p, seed=0)
+        b = 2 * g.total_memory
+        name = {0.2: "c5_p02", 0.3: "c5_p03"}.get(p, "random-dag")
+        gold = golden_run(fname, name, {"edge_prob": p} if name == "random-dag" else {}, "dp",
+                          lambda r: r["plan"]["budget"] == b)
+        guard(f"C5 p={p}", lambda: dict(exact_config(
+            f"C5 random-dag n=516 p={p} seed=0, exact DP, B=2M(V)"
+            + (" (north-star largest graph)" if p == 0.2 else ""),
+            g, b, world, local, reps if p != 0.2 else min(reps, 3), 1, pk, gold)))
+
+    # C1: ResNet-50, pruned, B = floor(vanilla peak / 2)
+    def c1():
+        g = named_graph("resnet50")
+        vp = simulate(g, liveness_pass(g, vanilla_schedule(g))).peak_live_memory
+        b = vp // 2
+        ms, plan = timed_calls(lambda: dp_plan(PlanRequest(g, b, "pruned")), world, reps)
+        gold = golden_run("named.json", "resnet50", {"vanilla_peak": vp}, "dp")
+        return {"config": "C1 ResNet-50 (n=176), pruned, minimize, B=floor(vanilla/2)",
+                "call": "dp_plan", "budget": b, "e2e_ms": ms,
+                "transitions": plan.stats.transitions, "parity": parity(plan, gold)}
+    guard("C1", c1)
+
+    # C2 search: U-Net skip 3, full family, min_feasible_budget
+    def c2():
+        g = named_graph("unet", skip_len=3)
+        ms, (b, plan) = timed_calls(lambda: min_feasible_budget(g, "full"), world, reps)
+        gold = golden_run("named.json", "unet", {"skip_len": 3}, "mfb",
+                          lambda r: r["family"] == "full")
+        par = parity(plan, gold["plan"] if gold else None)
+        if gold and b != gold["b_min"]:
+            par = f"MISMATCH: b_min {b} != {gold['b_min']}"
+        return {"config": "C2 U-Net skip_len=3 (F=2,726), full, min_feasible_budget",
+                "call": "min_feasible_budget", "b_min": b, "e2e_ms": ms, "parity": par}
+    guard("C2-search", c2)
+
+    # C3: DenseNet-161 memory-centric, both families
+    for fam in ("pruned", "full"):
+        def c3(fam=fam):
+            g = named_graph("densenet161")
+            ms, plan = timed_calls(lambda: memory_centric_plan(g, fam), world, reps)
+            gold = golden_run("named.json", "densenet161", {}, "mc",
+                              lambda r: r["family"] == fam)
+            return {"config": f"C3 DenseNet-161 (n=566), {fam}, memory_centric_plan",
+                    "call": "memory_centric_plan", "e2e_ms": ms,
+                    "objective_value": plan.objective_value,
+                    "parity": parity(plan, gold["plan"] if gold else None)}
+        guard(f"C3-{fam}", c3)
+
+    # C4: PSPNet 64-budget sweeps, budgets sharded over the ranks
+    for fam in ("pruned", "full"):
+        def c4(fam=fam):
+            g = named_graph("pspnet")
+            rec = next((r for r in _golden("bench_configs.json") if r["name"] == "pspnet_sweep"),
+                       None)
+            if rec:
+                budgets = rec["budgets"]
+            else:
+                vp = simulate(g, liveness_pass(g, vanilla_schedule(g))).peak_live_memory
+                bm, _ = min_feasible_budget(g, "pruned")
+                budgets = sweep_budgets(bm, vp if vp > bm else 2 * g.total_memory)
+            ms, plans = timed_calls(lambda: budget_sweep(g, budgets, fam), world, reps)
+            X = sum(p.stats.transitions for p in plans)
+            par = "no golden"
+            if rec and fam == "pruned":
+                bad = [b for p, r, b in zip(plans, rec["runs"], budgets)
+                       if parity(p, r["plan"]) != "bit-exact"]
+                par = "bit-exact (64 budgets)" if not bad else f"MISMATCH at budgets {bad[:4]}"
+            return {"config": f"C4 PSPNet (n=384), {fam}, 64-budget sweep",
+                    "call": "sweep.budget_sweep", "budgets": [budgets[0], budgets[-1]],
+                    "e2e_ms": ms, "transitions": X, "e2e_transitions_per_s": X / (ms / 1e3),
+                    "parallelism": f"budget-sharded x{world}" if world > 1 else "single GPU",
+                    "scaling": "strong" if world > 1 else None, "parity": par}
+        guard(f"C4-{fam}", c4)
+    return out
 
 
 def run_ours(args, world, rank, local):
@@ -241,169 +593,77 @@ def run_ours(args, world, rank, local):
 
     os.environ["REMAT_DEVICE"] = str(local)
     torch.cuda.set_device(local)
-    from paper_1905_11722_b200 import PlanRequest, dp_plan
-    from paper_1905_11722_b200._native import DeviceFamily, DeviceGraph, kernel_launches
-
-    g, name = workload(args)
-    levels = args.parallel == "levels"
-    if levels:
-        # level sharding: every rank works on the SAME solve (budget 2·M(V));
-        # each level's targets are split over the ranks, one NCCL all-gather
-        # per level (paper_1905_11722_b200/shard.py)
-        from paper_1905_11722_b200.shard import communicator
-
-        budget = 2 * g.total_memory
-        comm = communicator(local)
-    else:
-        # budget sharding: rank r solves budget 2·M(V) − r of the sweep (all
-        # budgets >= the single-segment need; per-rank work is near-identical)
-        budget = 2 * g.total_memory - rank
-    dg = DeviceGraph(g, local)
-    stream = torch.cuda.ExternalStream(dg.stream(), device=local)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-
-    def step():
-        fam = DeviceFamily(dg, "full", 2_000_000)
-        if levels:
-            info = fam.solve_level_sharded(comm, [budget], "minimize")[0][0]
-        else:
-            info = fam.solve([budget], "minimize")[0][0]
-        return fam, info
-
-    clocks = ClockSampler(local).__enter__()  # up and sampling before the timed region
-    # cold start: the process's first solve — lazy kernel-module
-    # load, first allocations, family build, relaxation — CUDA context excluded
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    step()
-    torch.cuda.synchronize()
-    cold_ms = (time.perf_counter() - t0) * 1e3
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    relax_ms = enum_ms = pre_ms = 0.0
-    relax_launches = 0
-    X = E = P = F = 0
-    launches0 = kernel_launches()
-    dev_ms = 0.0
-    clocks.start()
-    if True:
-        for k in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            barrier(world)
-            with torch.cuda.stream(stream):
-                ev[k][0].record(stream)
-                fam, info = step()
-                ev[k][1].record(stream)
-            torch.cuda.synchronize()
-            barrier(world)
-            t = fam.timings()
-            relax_ms += t["relax_ms"]
-            enum_ms += t["enumerate_ms"]
-            pre_ms += t["precompute_ms"]
-            relax_launches += t["relax_launches"]
-            X, E, P, F = (info.stats.transitions, info.stats.table_entries,
-                          t["comparable_pairs"], fam.size)
-            dev_ms += ev[k][0].elapsed_time(ev[k][1])
-            fam.close()
-    clocks.stop()
-    clocks.__exit__(None, None, None)
-    launches = kernel_launches() - launches0
-    ms_max = allmax(world, dev_ms)
-    # level sharding: all ranks share one solve, so its transitions count once
-    X_all = X * args.steps if levels else allsum(world, X * args.steps)
-    value = X_all / (ms_max / 1e3)
-
-    # end-to-end through the public API (graph in host memory, plan back on host)
     from paper_1905_11722_b200.graph import pack_graph
 
+    g, name, budget = headline(args)
+    pk = peaks()
+    clocks = ClockSampler(local).__enter__()  # sampling before the timed region
+    # cold start: the process's first solve (lazy module load, first
+    # allocations), CUDA context excluded
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ds = DeviceSolve(g, local, world, budget)
+    ds.once()[0].close()
+    torch.cuda.synchronize()
+    cold_ms = (time.perf_counter() - t0) * 1e3
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    r = ds.timed(args.steps, args.warmup, flush=flush, clocks=clocks)
+    launches = r["launches"]
+    clocks.__exit__(None, None, None)
+    ds.close()
+    info = r["info"]
+    X, E, P, F = (info.stats.transitions, info.stats.table_entries, r["P"], r["F"])
+    value = X / (r["ms"] / 1e3)
+
+    e2e_s, plan = e2e_exact(g, budget, world, max(1, min(args.steps, 5)))
     _, _, pr, su, tc, mc = pack_graph(g)
     h2d = pr.nbytes + su.nbytes + tc.nbytes + mc.nbytes
-    e2e_t = []
-    for k in range(max(1, min(args.steps, 5))):
-        barrier(world)
-        t0 = time.perf_counter()
-        plan = dp_plan(PlanRequest(g, budget, "full", "minimize"))
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_s = allmax(world, sum(e2e_t) / len(e2e_t))
-    e2e_value = allsum(world, plan.stats.transitions) / e2e_s
-    if levels:  # the public API of the level-sharded path
-        from paper_1905_11722_b200.shard import LevelShardedSolver
-
-        e2e_t = []
-        for k in range(max(1, min(args.steps, 5))):
-            barrier(world)
-            t0 = time.perf_counter()
-            ls = LevelShardedSolver(g, "full")
-            plan = ls.plan(budget)
-            ls.close()
-            e2e_t.append(time.perf_counter() - t0)
-        e2e_s = allmax(world, sum(e2e_t) / len(e2e_t))
-        e2e_value = plan.stats.transitions / e2e_s
     d2h = (g.n + 1) * 8 * ((g.n + 63) // 64) * 2 + (g.n + 1) * 8 + 64
+    gold = golden_run("oracle_large.json", "unet_c8", {}, "dp",
+                      lambda x: x["plan"]["budget"] == budget) if args.skip_len == 8 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = len(os.sched_getaffinity(0))
-        dt, r = cpu_port(g, budget, threads)
-        assert r["objective_value"] == plan.objective_value
-        assert r["stats"]["transitions"] == plan.stats.transitions
-        cpu = {"value": r["stats"]["transitions"] / dt, "unit": "transitions/s", "cores": threads,
-               "kind": "port", "sample": "one full dp_plan of the workload (oracle/remat_oracle.c, "
-                                         f"OpenMP, {dt:.1f} s)"}
+        dt, ref = cpu_port(g, budget, threads)
+        assert ref["objective_value"] == plan.objective_value
+        assert ref["stats"]["transitions"] == plan.stats.transitions
+        cpu = {"value": ref["stats"]["transitions"] / dt, "unit": "transitions/s",
+               "cores": threads, "kind": "port",
+               "sample": f"one full dp_plan of the workload (oracle/remat_oracle.c, OpenMP, "
+                         f"{dt:.1f} s)",
+               "python_reference": python_reference_sample()}
+    configs = [] if args.no_configs else other_configs(args, world, rank, local, pk)
     if rank != 0:
         return
-    pk = peaks()
-    q_relax = q_alg_relax(g.n, X, P, E)
-    relax_s = relax_ms / 1e3 / args.steps
-    achieved = q_relax / relax_s / 1e9
+    ph = r["phases"]
     prof = ROOT / "profiles" / "relax_traffic.json"
     traffic = None
     if prof.exists():  # ncu capture of the same workload (tools/gpu_traffic.sh)
         rec = json.loads(prof.read_text()).get(name)
-        if rec:
-            traffic = rec["dram_bytes_per_launch"]
-    issue = None
-    prof_i = ROOT / "profiles" / "relax_issue.json"
-    if prof_i.exists():  # ncu capture of the heaviest launch + measured issue peak
-        issue = json.loads(prof_i.read_text()).get(name)
+        traffic = rec["dram_bytes_per_launch"] if rec else None
     line = {
-        "metric": "exact-DP transitions/s (end-to-end solve)",
-        "value": value, "unit": "transitions/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "strong" if levels else "weak", "vs_baseline": None,
-        "dtype": "int64", "data": "synthetic",
-        "config": {"workload": name, "n": g.n, "family_size": F, "budget": budget,
-                   "transitions_per_step": X, "comparable_pairs": P, "table_entries": E,
-                   "parallelism": (f"level-sharded x{world} (NCCL all-gather per level)" if levels
-                                   else f"budget-sharded x{world}" if world > 1 else "single GPU"),
-                   "l2": "flushed (256 MiB write) between steps",
-                   "phase_ms": {"enumerate": enum_ms / args.steps,
-                                "precompute": pre_ms / args.steps,
-                                "relax": relax_ms / args.steps}},
-        "roofline": {"bound": "hbm", "kernel": "k_relax_tile",
-                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic,
-                     "peak_source": pk["source"],
-                     "bytes_per_launch": q_relax / max(1, relax_launches // args.steps),
-                     "avg_launch_ms": relax_ms / max(1, relax_launches),
-                     "note": ("achieved = SURVEY 8(d) algorithmic bytes 12X+(16W+16)P+16E of the "
-                              "relaxation / its device time; the table is L2-resident (traffic = "
-                              "measured DRAM bytes per launch), so the binding resource is SM "
-                              "issue (see `issue`: executed IPC of the heaviest launch against "
-                              "the measured 4-slot issue peak, tools/micro/pipes.cu)"),
-                     "issue": issue},
+        "metric": METRIC, "value": value, "unit": "transitions/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms"],
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": config_of(name, g, budget, F, X, P, E),
+        "parallelism": (f"level-sharded x{world} (NCCL all-gather per level)" if world > 1
+                        else "single GPU"),
+        "phase_ms": {"enumerate": ph["enumerate_ms"], "precompute": ph["precompute_ms"],
+                     "relax": ph["relax_ms"]},
+        "parity": parity(plan, gold["plan"] if gold else None),
+        "roofline": relax_roofline(g.n, X, P, E, ph["relax_ms"] / 1e3, ph["relax_launches"], pk,
+                                   traffic),
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "transitions/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s},
+        "e2e": {"value": plan.stats.transitions / e2e_s, "unit": "transitions/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "seconds_per_step": e2e_s},
         "gpu_launches": launches,
         "cold_start": {"ms": cold_ms, "what": "first solve of the process (lazy module load, "
-                                              "allocations, family build, relaxation); CUDA "
-                                              "context creation excluded; not in `value`"},
+                                              "allocations); CUDA context excluded; not in value"},
         "clocks": clocks.summary(),
+        "configs": configs,
     }
     print(json.dumps(line), flush=True)
 
@@ -414,13 +674,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--workload", choices=("unet", "random-dag"), default="unet")
     ap.add_argument("--skip-len", type=int, default=8)
-    ap.add_argument("--edge-prob", type=float, default=0.3)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--parallel", choices=("budgets", "levels"), default="budgets",
-                    help="N>1: independent budgets per GPU (weak) or one solve with every "
-                         "level's targets sharded over the GPUs (strong)")
+    ap.add_argument("--no-configs", action="store_true", help="headline only")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

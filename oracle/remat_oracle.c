@@ -11,6 +11,8 @@
 #include "remat_oracle.h"
 
 #include <limits.h>
+#include <stdio.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -18,6 +20,12 @@
 #endif
 
 #define EMPTY INT64_MAX
+
+static double now_s(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
 
 /* ------------------------------------------------------------------------ */
 /* set algebra (graph.py:117-164)                                            */
@@ -300,6 +308,45 @@ typedef struct {
   int64_t stage_fixed, dt, dm;
 } pair_t;
 
+/* A cost vector restated as K weight classes: cost(S) = Σ_k value_k·|S ∩ C_k|
+ * (an identity for any S when C_k = {v : cost_v = value_k}).  Used only when
+ * the graph has ≤ 8 distinct costs; otherwise the bit loop of weight_of. */
+typedef struct {
+  int k;              /* 0 = not usable */
+  int64_t value[8];
+  uint64_t *mask;     /* [k][w] */
+} wclass;
+
+static void wclass_init(wclass *c, const int64_t *cost, int n, int w) {
+  c->k = 0;
+  c->mask = NULL;
+  int k = 0;
+  for (int v = 0; v < n; v++) {
+    int f = 0;
+    for (int q = 0; q < k; q++) f |= c->value[q] == cost[v];
+    if (f) continue;
+    if (k == 8) return;
+    c->value[k++] = cost[v];
+  }
+  c->mask = calloc((size_t)(k ? k : 1) * w, sizeof(uint64_t));
+  for (int v = 0; v < n; v++)
+    for (int q = 0; q < k; q++)
+      if (c->value[q] == cost[v]) c->mask[(size_t)q * w + (v >> 6)] |= 1ull << (v & 63);
+  c->k = k;
+}
+
+static int64_t wclass_weight(const wclass *c, const int64_t *cost, const uint64_t *s, int w) {
+  if (!c->k) return weight_of(cost, s, w);
+  int64_t acc = 0;
+  for (int q = 0; q < c->k; q++) {
+    const uint64_t *m = c->mask + (size_t)q * w;
+    int64_t cnt = 0;
+    for (int k = 0; k < w; k++) cnt += __builtin_popcountll(s[k] & m[k]);
+    acc += c->value[q] * cnt;
+  }
+  return acc;
+}
+
 typedef struct {
   const orc_graph *g;
   maskvec fam;
@@ -307,6 +354,7 @@ typedef struct {
   int64_t *stage_base; /* M(δ+(L)\L) + M(δ−(δ+(L))\L)           (110-115) */
   int64_t empty_index, full_index;
   pair_t **rows;       /* cached successor rows (NULL = not built) */
+  wclass tcls, mcls;   /* T / M as weighted popcounts when few distinct costs */
   int32_t *row_len;
   int64_t cached_bytes, cache_limit;
 } tindex;
@@ -324,6 +372,10 @@ static int index_init(tindex *ix, const orc_graph *g, maskvec fam) {
   ix->row_len = calloc(F, sizeof(int32_t));
   ix->cached_bytes = 0;
   ix->cache_limit = (int64_t)8 << 30;
+  const char *lim = getenv("ORC_INDEX_CACHE_BYTES"); /* tests force the lazy path */
+  if (lim) ix->cache_limit = atoll(lim);
+  wclass_init(&ix->tcls, g->tcost, g->n, w);
+  wclass_init(&ix->mcls, g->mcost, g->n, w);
   if (!ix->bound || !ix->stage_base || !ix->rows || !ix->row_len) return ORC_ERR_NOMEM;
 #pragma omp parallel
   {
@@ -353,7 +405,27 @@ static void index_free(tindex *ix) {
   free(ix->row_len);
   free(ix->bound);
   free(ix->stage_base);
+  free(ix->tcls.mask);
+  free(ix->mcls.mask);
   free(ix->fam.masks);
+}
+
+/* Pair constants of L_i ⊆ L_j from their definitions (planner.py:124-131):
+ * stage_fixed = 2·M(L_j\L_i) + stage_base[j], dt = T((L_j\L_i)\∂L_j),
+ * dm = M(∂L_j\L_i). */
+static void pair_constants(const tindex *ix, int64_t i, int64_t j, uint64_t *seg,
+                           uint64_t *tmp, pair_t *p) {
+  const orc_graph *g = ix->g;
+  int w = g->w;
+  const uint64_t *lo = ix->fam.masks + i * w, *hi = ix->fam.masks + j * w;
+  const uint64_t *bj = ix->bound + j * w;
+  for (int k = 0; k < w; k++) seg[k] = hi[k] & ~lo[k];
+  p->j = (int32_t)j;
+  p->stage_fixed = 2 * wclass_weight(&ix->mcls, g->mcost, seg, w) + ix->stage_base[j];
+  for (int k = 0; k < w; k++) tmp[k] = seg[k] & ~bj[k];
+  p->dt = wclass_weight(&ix->tcls, g->tcost, tmp, w);
+  for (int k = 0; k < w; k++) tmp[k] = bj[k] & ~lo[k];
+  p->dm = wclass_weight(&ix->mcls, g->mcost, tmp, w);
 }
 
 /* Successor row of member i: every j > i with L_i ⊆ L_j, with the reference's
@@ -372,18 +444,7 @@ static int32_t build_row(const tindex *ix, int64_t i, pair_t *row) {
     int sub = 1;
     for (int k = 0; k < w && sub; k++) sub = (lo[k] & ~hi[k]) == 0;
     if (!sub) continue;
-    if (row) {
-      const uint64_t *bj = ix->bound + j * w;
-      for (int k = 0; k < w; k++) seg[k] = hi[k] & ~lo[k];
-      pair_t p;
-      p.j = (int32_t)j;
-      p.stage_fixed = 2 * weight_of(g->mcost, seg, w) + ix->stage_base[j];
-      for (int k = 0; k < w; k++) tmp[k] = seg[k] & ~bj[k];
-      p.dt = weight_of(g->tcost, tmp, w);
-      for (int k = 0; k < w; k++) tmp[k] = bj[k] & ~lo[k];
-      p.dm = weight_of(g->mcost, tmp, w);
-      row[cnt] = p;
-    }
+    if (row) pair_constants(ix, i, j, seg, tmp, &row[cnt]);
     cnt++;
   }
   return cnt;
@@ -412,15 +473,6 @@ static int index_materialise(tindex *ix) {
   return ORC_OK;
 }
 
-static pair_t *index_row(tindex *ix, int64_t i, int32_t *len, int *owned) {
-  if (ix->rows[i]) { *len = ix->row_len[i]; *owned = 0; return ix->rows[i]; }
-  int32_t cnt = ix->row_len[i];
-  pair_t *row = malloc(sizeof(pair_t) * (cnt ? cnt : 1));
-  if (row) build_row(ix, i, row);
-  *len = cnt;
-  *owned = 1;
-  return row;
-}
 
 /* ------------------------------------------------------------------------ */
 /* strategy.py: make_sequence + peak_memory                                  */
@@ -544,10 +596,40 @@ static int plan_with_index(tindex *ix, int64_t budget, int objective, orc_plan *
     }
     if (!have) continue;
     st.states_visited += nf;
-    int32_t rl;
-    int owned;
-    pair_t *row = index_row(ix, i, &rl, &owned);
-    if (!row) { rc = ORC_ERR_NOMEM; break; }
+    if (!ix->rows[i]) {
+      /* lazy row (index too large to cache): the pair scan of build_row fused
+       * with the relaxation, parallel over j (each target j has one writer) */
+      int64_t cnt = 0;
+#pragma omp parallel for schedule(dynamic, 256) reduction(+ : cnt)
+      for (int64_t j = i + 1; j < F; j++) {
+        const uint64_t *lo = ix->fam.masks + i * w, *hi = ix->fam.masks + j * w;
+        int sub = 1;
+        for (int k = 0; k < w && sub; k++) sub = (lo[k] & ~hi[k]) == 0;
+        if (!sub) continue;
+        uint64_t seg[64], tmp[64];
+        pair_t p;
+        pair_constants(ix, i, j, seg, tmp, &p);
+        cnt++;
+        TOUCH(j);
+        int64_t *target = opt[j];
+        for (int64_t e = 0; e < nf; e++) {
+          int64_t m = fm[e];
+          if (m + p.stage_fixed > budget) continue;
+          int64_t t2 = ft[e] + p.dt;
+          int64_t m2 = m + p.dm;
+          if (m2 < target[t2]) {
+            target[t2] = m2;
+            par_i[j][t2] = (int32_t)i;
+            par_t[j][t2] = (int32_t)ft[e];
+          }
+        }
+      }
+      pairs += cnt;
+      st.transitions += nf * cnt; /* counted before the budget test (164) */
+      continue;
+    }
+    int32_t rl = ix->row_len[i];
+    pair_t *row = ix->rows[i];
     pairs += rl;
     st.transitions += nf * (int64_t)rl; /* counted before the budget test (164) */
     for (int32_t r = 0; r < rl; r++) TOUCH(row[r].j);
@@ -568,7 +650,6 @@ static int plan_with_index(tindex *ix, int64_t budget, int objective, orc_plan *
         }
       }
     }
-    if (owned) free(row);
   }
   /* cells created by a passing transition are never empty (171-174) */
   for (int64_t i = 0; i < F; i++) {
@@ -646,8 +727,13 @@ int orc_dp_plan(const orc_graph *g, int family, int64_t cap, int64_t budget,
   if (rc) return rc;
   tindex ix;
   memset(&ix, 0, sizeof ix);
+  double t0 = now_s();
   rc = index_init(&ix, g, fam);
+  double t1 = now_s();
   if (!rc) rc = plan_with_index(&ix, budget, objective, out);
+  if (getenv("ORC_VERBOSE"))
+    fprintf(stderr, "orc_dp_plan: F=%lld index %.3f s, dp %.3f s\n", (long long)fam.count,
+            t1 - t0, now_s() - t1);
   index_free(&ix);
   return rc;
 }

@@ -9,7 +9,8 @@ Every fixture stores the graph as the reference's own ``graph_to_document``
 (index order) plus the reference's outputs for it.  Node sets are written as
 hex strings.  ``--slow`` adds the named-shape cases whose reference solve takes
 minutes (C3 DenseNet-161, C5 random-dag n=516 p=0.5); ``--xslow`` writes
-named_xslow.json (C5 p=0.4, memory-centric U-Net; ~10 min).
+named_xslow.json (C5 p=0.4, memory-centric U-Net; ~10 min); ``--bench`` writes
+bench_configs.json (the C4 PSPNet 64-budget sweep that bench.py checks).
 
 Fixtures (all keyed on reference call sites, file:line under pkg/src/remat):
   dp_corpus.json     dp_plan (planner.py:214) on seeded random DAGs, both
@@ -415,6 +416,27 @@ def named_xslow():
     return out
 
 
+def bench_configs():
+    """Reference outputs for the bench.py workloads the reference finishes:
+    C4 — PSPNet, pruned family, the 64-budget sweep B_k = B_min +
+    ⌊k·(V_peak − B_min)/63⌋, each budget one dp_plan."""
+    out = []
+    g = graph_from_document(ours.pspnet_document())
+    vp = vanilla_peak(g)
+    b_min, _ = min_feasible_budget(g, "pruned")
+    top = vp if vp > b_min else 2 * g.total_memory
+    budgets = [b_min + (k * (top - b_min)) // 63 for k in range(64)]
+    rec = {"name": "pspnet_sweep", "kw": {"vanilla_peak": vp, "b_min": b_min},
+           "graph": graph_to_document(g), "budgets": budgets, "runs": []}
+    t0 = time.perf_counter()
+    for b in budgets:
+        rec["runs"].append({"kind": "dp", "plan": plan_json(dp_plan(PlanRequest(g, b, "pruned")))})
+    rec["ref_seconds"] = round(time.perf_counter() - t0, 3)
+    print(f"  C4 sweep: {rec['ref_seconds']}s", flush=True)
+    out.append(rec)
+    return out
+
+
 def dump(name: str, obj) -> None:
     path = OUT / name
     path.write_text(json.dumps(obj, separators=(",", ":")) + "\n")
@@ -435,6 +457,8 @@ def main() -> None:
     }
     if "--xslow" in sys.argv:
         jobs = {"named_xslow.json": named_xslow}
+    if "--bench" in sys.argv:
+        jobs = {"bench_configs.json": bench_configs}
     for fname, fn in jobs.items():
         if only and fname not in only:
             continue

@@ -44,6 +44,9 @@ def test_reference_arm_line():
     assert line["e2e"]["value"] == line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == line["e2e"]["d2h_bytes_per_step"] == 0
     assert line["config"]["transitions_per_step"] > 0
+    py = line["cpu_baseline"]["python_reference"]
+    if (ROOT / "oracle" / "_ref" / "remat").is_dir():
+        assert py["kind"] == "reference" and py["cores"] == 1 and py["value"] > 0
 
 
 def test_reference_arm_under_torchrun_prints_once():
@@ -60,8 +63,8 @@ def test_reference_arm_under_torchrun_prints_once():
 @pytest.mark.gpu
 def test_our_arm_line():
     r = subprocess.run([sys.executable, "bench.py", "--skip-len", "3", "--steps", "3",
-                        "--warmup", "3", "--no-cpu"], cwd=ROOT, capture_output=True, text=True,
-                       timeout=600, env=_env())
+                        "--warmup", "3", "--no-cpu", "--no-configs"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600, env=_env())
     assert r.returncode == 0, r.stderr[-2000:]
     (line,) = _lines(r.stdout)
     assert BASE_KEYS <= set(line)
@@ -70,3 +73,22 @@ def test_our_arm_line():
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(line["roofline"])
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
+
+
+@pytest.mark.gpu
+def test_our_arm_configs_are_timed_and_bit_exact():
+    """Every BASELINE config rides in the bench line, each checked against its
+    committed golden (reference or pinned-oracle outputs)."""
+    r = subprocess.run([sys.executable, "bench.py", "--skip-len", "3", "--steps", "1",
+                        "--warmup", "3", "--no-cpu"], cwd=ROOT, capture_output=True, text=True,
+                       timeout=900, env=_env())
+    assert r.returncode == 0, r.stderr[-2000:]
+    (line,) = _lines(r.stdout)
+    cfgs = line["configs"]
+    assert len(cfgs) >= 8
+    for c in cfgs:
+        assert "error" not in c, c
+        assert not c["parity"].startswith("MISMATCH"), c
+    c5 = cfgs[0]
+    assert "p=0.2" in c5["config"] and c5["transitions"] > 10**10
+    assert c5["roofline"]["frac"] > 0
