@@ -14,7 +14,7 @@ from pathlib import Path
 
 import numpy as np
 
-from .graph import GraphError, pack_graph
+from .graph import GraphError, array_to_masks, masks_to_array, pack_graph
 
 # REMAT_B200_LIB: an alternative build of the same library (A/B runs of kernel variants)
 LIB_PATH = Path(os.environ.get("REMAT_B200_LIB") or
@@ -162,7 +162,7 @@ def kernel_launches() -> int:
     return int(lib().remat_kernel_launch_count())
 
 
-def _default_device() -> int:
+def default_device() -> int:
     env = os.environ.get("REMAT_DEVICE")
     if env is not None:
         return int(env)
@@ -176,14 +176,23 @@ def _default_device() -> int:
     return 0
 
 
+def _live(h, what: str):
+    if h is None:
+        raise ValueError(f"{what} is closed")
+    return h
+
+
 class DeviceGraph:
-    """A graph resident on one GPU (owns a ``remat_graph_t``)."""
+    """A graph resident on one GPU (owns a ``remat_graph_t``).  Calls on one
+    handle are serialised (its stream and scratch buffers are shared)."""
 
     def __init__(self, g, device: int | None = None):
-        n, w, preds, succs, tcost, mcost = pack_graph(g)
+        packed = getattr(g, "packed", None)
+        n, w, preds, succs, tcost, mcost = packed if packed is not None else pack_graph(g)
+        self.lock = threading.Lock()
         self.graph = g
         self.n, self.w = n, w
-        self.device = _default_device() if device is None else device
+        self.device = default_device() if device is None else device
         h = _P()
         check(lib().remat_graph_create(self.device, n, preds.ctypes.data, succs.ctypes.data,
                                        tcost.ctypes.data, mcost.ctypes.data, C.byref(h)))
@@ -191,7 +200,7 @@ class DeviceGraph:
 
     def stream(self) -> int:
         s = _P()
-        check(lib().remat_graph_stream(self.handle, C.byref(s)))
+        check(lib().remat_graph_stream(_live(self.handle, "graph handle"), C.byref(s)))
         return s.value or 0
 
     def close(self):
@@ -209,18 +218,16 @@ class DeviceGraph:
 
     def evaluate(self, chain: list[int]):
         k = len(chain)
-        buf = np.zeros((max(k, 1), self.w), dtype=np.uint64)
-        for s, m in enumerate(chain):
-            for q in range(self.w):
-                buf[s, q] = (m >> (64 * q)) & 0xFFFFFFFFFFFFFFFF
+        buf = masks_to_array(chain, self.w) if k else np.zeros((1, self.w), dtype=np.uint64)
         stage = np.zeros(max(k, 1), dtype=np.int64)
         cached = np.zeros((max(k, 1), self.w), dtype=np.uint64)
         ovh, peak, ctot = _I64(), _I64(), _I64()
-        check(lib().remat_evaluate(self.handle, k, buf.ctypes.data, C.byref(ovh),
-                                   stage.ctypes.data, C.byref(peak), C.byref(ctot),
-                                   cached.ctypes.data))
-        return ovh.value, [int(x) for x in stage[:k]], peak.value, ctot.value, [
-            words_to_int(cached[s]) for s in range(k)]
+        with self.lock:
+            check(lib().remat_evaluate(_live(self.handle, "graph handle"), k, buf.ctypes.data,
+                                       C.byref(ovh), stage.ctypes.data, C.byref(peak),
+                                       C.byref(ctot), cached.ctypes.data))
+        return ovh.value, [int(x) for x in stage[:k]], peak.value, ctot.value, \
+            array_to_masks(cached[:k])
 
     def simulate(self, schedules: list[np.ndarray], want_trace: bool = True):
         offs = np.zeros(len(schedules) + 1, dtype=np.int64)
@@ -233,9 +240,10 @@ class DeviceGraph:
                 flat[offs[s]:offs[s + 1]] = ops
         infos = (SimInfo * len(schedules))()
         trace = np.zeros(max(total, 1), dtype=np.int64)
-        check(lib().remat_simulate(self.handle, len(schedules), offs.ctypes.data,
-                                   flat.ctypes.data, C.addressof(infos),
-                                   trace.ctypes.data if want_trace else None))
+        with self.lock:
+            check(lib().remat_simulate(_live(self.handle, "graph handle"), len(schedules),
+                                       offs.ctypes.data, flat.ctypes.data, C.addressof(infos),
+                                       trace.ctypes.data if want_trace else None))
         return infos, offs, trace
 
 
@@ -299,8 +307,8 @@ class DeviceFamily:
         self.family = family
         self.cap = cap
         h = _P()
-        check(lib().remat_family_create(dg.handle, FAMILY_CODE[family], int(cap), C.byref(h)),
-              cap=cap)
+        check(lib().remat_family_create(_live(dg.handle, "graph handle"), FAMILY_CODE[family],
+                                        int(cap), C.byref(h)), cap=cap)
         self.handle = h
         sz = _I64()
         check(lib().remat_family_size(h, C.byref(sz)))
@@ -321,12 +329,13 @@ class DeviceFamily:
         if count is None:
             count = self.size - start
         buf = np.zeros((max(count, 1), self.dg.w), dtype=np.uint64)
-        check(lib().remat_family_masks(self.handle, start, count, buf.ctypes.data))
-        return [words_to_int(buf[i]) for i in range(count)]
+        check(lib().remat_family_masks(_live(self.handle, "family handle"), start, count,
+                                       buf.ctypes.data))
+        return array_to_masks(buf[:count])
 
     def timings(self) -> dict:
         t = Timings()
-        check(lib().remat_family_timings(self.handle, C.byref(t)))
+        check(lib().remat_family_timings(_live(self.handle, "family handle"), C.byref(t)))
         return {k: getattr(t, k) for k, _ in Timings._fields_}
 
     def _alloc(self, nb: int):
@@ -350,7 +359,8 @@ class DeviceFamily:
         b = np.asarray([min(int(x), 2**62) for x in budgets], dtype=np.int64)
         infos = (PlanInfo * nb)()
         chain, cached, stage = self._alloc(nb)
-        check(lib().remat_solve(self.handle, b.ctypes.data, nb, OBJECTIVE_CODE[objective],
+        check(lib().remat_solve(_live(self.handle, "family handle"), b.ctypes.data, nb,
+                                OBJECTIVE_CODE[objective],
                                 C.addressof(infos), chain.ctypes.data, cached.ctypes.data,
                                 stage.ctypes.data))
         return [self._unpack(infos[i], chain[i], cached[i], stage[i]) for i in range(nb)]
@@ -367,14 +377,16 @@ class DeviceFamily:
     def solve_level_sharded(self, comm: "Comm", budgets: list[int], objective: str):
         """``solve`` with every level's targets split over the communicator's ranks."""
         return self._solve_with(
-            lambda *a: lib().remat_solve_level_sharded(self.handle, comm.handle, *a),
+            lambda *a: lib().remat_solve_level_sharded(_live(self.handle, "family handle"),
+                                                       _live(comm.handle, "communicator"), *a),
             budgets, objective)
 
     def min_feasible_budget(self, objective: str, probes_per_round: int = 8):
         info = PlanInfo()
         chain, cached, stage = self._alloc(1)
         bmin, probes, ptrans = _I64(), _I64(), _I64()
-        check(lib().remat_min_feasible_budget(self.handle, OBJECTIVE_CODE[objective],
+        check(lib().remat_min_feasible_budget(_live(self.handle, "family handle"),
+                                              OBJECTIVE_CODE[objective],
                                               probes_per_round, C.byref(bmin), C.byref(info),
                                               chain.ctypes.data, cached.ctypes.data,
                                               stage.ctypes.data, C.byref(probes),
@@ -385,7 +397,5 @@ class DeviceFamily:
     @staticmethod
     def _unpack(info, chain, cached, stage):
         k = info.k if info.status == OK else 0
-        return (info,
-                [words_to_int(chain[s]) for s in range(k)],
-                [words_to_int(cached[s]) for s in range(k)],
+        return (info, array_to_masks(chain[:k]), array_to_masks(cached[:k]),
                 [int(x) for x in stage[:k]])

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -18,15 +19,31 @@ namespace remat {
 static thread_local std::string g_last_error;
 thread_local cudaStream_t tls_stream = nullptr;
 
-void prepare_pool(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    unsigned long long keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+thread_local cudaMemPool_t tls_pool = nullptr;
+
+cudaMemPool_t prepare_pool(int device) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[kMaxDevices] = {};
+  const int d = dev_slot(device);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!pools[d]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      cudaDeviceGetDefaultMemPool(&pool, device);  // cannot happen on sm_100; stay usable
+    } else {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pools[d] = pool;
   }
-  done[device] = true;
+  tls_pool = pools[d];
+  return pools[d];
 }
 int sm_count(int device) {
   static std::atomic<int> sms[kMaxDevices] = {};
@@ -207,7 +224,10 @@ int remat_device_count(int32_t* count) {
 int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const uint64_t* succs,
                        const int64_t* compute_costs, const int64_t* memory_costs,
                        remat_graph_t* out) {
+  if (!out) return fail(REMAT_ERR_VALUE, "null output pointer");
   *out = nullptr;
+  if (!preds || !succs || !compute_costs || !memory_costs)
+    return fail(REMAT_ERR_VALUE, "null graph array");
   if (n < 1) return fail(REMAT_ERR_VALUE, "graph must have at least one node");
   const int W = (n + 63) / 64;
   const int Wp = padded_words(W);
@@ -225,9 +245,6 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
   }
   if (MV > (1LL << 61))
     return fail(REMAT_ERR_RANGE, "total memory cost must stay below 2^61 (2*M(V) stage bound)");
-  if (TV + 1 > (1LL << 24))
-    return fail(REMAT_ERR_RANGE, "total compute cost T(V) = " + std::to_string(TV) +
-                                     " exceeds the dense overhead-row limit 2^24-1");
   int rc = set_device(device);
   if (rc < 0) return rc;
   auto* g = new remat_graph_s();
@@ -286,12 +303,15 @@ int remat_graph_free(remat_graph_t g) {
 }
 
 int remat_graph_stream(remat_graph_t g, void** stream) {
+  if (!g) return fail(REMAT_ERR_VALUE, "null graph handle");
   *stream = (void*)g->stream;
   return REMAT_OK;
 }
 
 int remat_family_create(remat_graph_t g, int32_t kind, int64_t cap, remat_family_t* out) {
+  if (!out) return fail(REMAT_ERR_VALUE, "null output pointer");
   *out = nullptr;
+  if (!g) return fail(REMAT_ERR_VALUE, "null graph handle");
   if (kind != REMAT_FAMILY_FULL && kind != REMAT_FAMILY_PRUNED)
     return fail(REMAT_ERR_VALUE, "family must be full (0) or pruned (1)");
   if (kind == REMAT_FAMILY_FULL && cap < (int64_t)g->n + 1)
@@ -313,11 +333,13 @@ int remat_family_create(remat_graph_t g, int32_t kind, int64_t cap, remat_family
 }
 
 int remat_family_size(remat_family_t f, int64_t* size) {
+  if (!f) return fail(REMAT_ERR_VALUE, "null family handle");
   *size = f->F;
   return REMAT_OK;
 }
 
 int remat_family_masks(remat_family_t f, int64_t start, int64_t count, uint64_t* out) {
+  if (!f) return fail(REMAT_ERR_VALUE, "null family handle");
   if (start < 0 || count < 0 || start + count > f->F)
     return fail(REMAT_ERR_VALUE, "family index range out of bounds");
   remat_graph_s* g = f->g;
@@ -337,12 +359,17 @@ int remat_family_masks(remat_family_t f, int64_t start, int64_t count, uint64_t*
 
 int remat_family_free(remat_family_t f) {
   if (!f) return REMAT_OK;
-  set_device(f->g->device, f->g->stream);
+  remat_graph_s* g = f->g;
+  set_device(g->device, g->stream);
   delete f;
+  // return what a large family held beyond the pool's working set
+  cudaStreamSynchronize(g->stream);
+  cudaMemPoolTrimTo(tls_pool, kPoolKeepBytes);
   return REMAT_OK;
 }
 
 int remat_family_timings(remat_family_t f, remat_timings* out) {
+  if (!f) return fail(REMAT_ERR_VALUE, "null family handle");
   *out = f->timings;
   return REMAT_OK;
 }
@@ -350,6 +377,8 @@ int remat_family_timings(remat_family_t f, remat_timings* out) {
 int remat_solve(remat_family_t f, const int64_t* budgets, int32_t nb, int32_t objective,
                 remat_plan_info* info, uint64_t* chain_masks, uint64_t* cached_masks,
                 int64_t* stage_memory) {
+  if (!f) return fail(REMAT_ERR_VALUE, "null family handle");
+  if (!budgets || !info) return fail(REMAT_ERR_VALUE, "null budget or result array");
   if (nb < 1) return fail(REMAT_ERR_VALUE, "need at least one budget");
   if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
     return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
@@ -379,6 +408,7 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
                               int64_t* b_min, remat_plan_info* info, uint64_t* chain_masks,
                               uint64_t* cached_masks, int64_t* stage_memory,
                               int64_t* probes_run, int64_t* probe_transitions) {
+  if (!f || !b_min || !info) return fail(REMAT_ERR_VALUE, "null family handle or output");
   if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
     return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
   remat_graph_s* g = f->g;
@@ -452,6 +482,8 @@ int remat_min_feasible_budget(remat_family_t f, int32_t objective, int32_t probe
 int remat_evaluate(remat_graph_t g, int32_t k, const uint64_t* chain, int64_t* overhead,
                    int64_t* stage_memory, int64_t* peak, int64_t* cached_total,
                    uint64_t* cached_masks) {
+  if (!g || !chain || !overhead || !peak || !cached_total)
+    return fail(REMAT_ERR_VALUE, "null graph handle or argument");
   const int n = g->n, W = g->W, Wp = g->Wp;
   if (k < 1 || k > n) return fail(REMAT_ERR_VALUE, "chain length must be in [1, n]");
   int rc = set_device(g->device, g->stream);
@@ -492,6 +524,7 @@ int remat_evaluate(remat_graph_t g, int32_t k, const uint64_t* chain, int64_t* o
 
 int remat_simulate(remat_graph_t g, int32_t nsched, const int64_t* offsets, const int32_t* ops,
                    remat_sim_info* info, int64_t* traces) {
+  if (!g || !offsets || !ops || !info) return fail(REMAT_ERR_VALUE, "null graph handle or argument");
   if (nsched < 1) return fail(REMAT_ERR_VALUE, "need at least one schedule");
   int rc = set_device(g->device, g->stream);
   if (rc < 0) return rc;

@@ -386,12 +386,12 @@ __global__ void k_scan_add(long long* __restrict__ out, long long n,
 static int scan_rec(const long long* in, long long* out, long long n, cudaStream_t s) {
   long long nb = (n + 1023) / 1024;
   long long* sums = nullptr;
-  RM_CUDA(cudaMallocAsync(&sums, sizeof(long long) * (nb + 1), s));
+  RM_CUDA(cudaMallocFromPoolAsync(&sums, sizeof(long long) * (nb + 1), tls_pool, s));
   k_scan_block<<<(unsigned)nb, 1024, 0, s>>>(in, out, n, sums);
   RM_LAUNCHED();
   if (nb > 1) {
     long long* soff = nullptr;
-    RM_CUDA(cudaMallocAsync(&soff, sizeof(long long) * (nb + 1), s));
+    RM_CUDA(cudaMallocFromPoolAsync(&soff, sizeof(long long) * (nb + 1), tls_pool, s));
     int rc = scan_rec(sums, soff, nb, s);
     if (rc < 0) return rc;
     k_scan_add<<<(unsigned)nb, 1024, 0, s>>>(out, n, soff);
@@ -838,6 +838,10 @@ static int build_family_w(remat_graph_s* g, int kind, long long cap, remat_famil
 }
 
 int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
+  // the DP keeps a dense overhead row per member (capacity T(L)+1, 32-bit t)
+  if (g->TV + 1 > (1LL << 24))
+    return fail(REMAT_ERR_RANGE, "total compute cost T(V) = " + std::to_string(g->TV) +
+                                     " exceeds the dense overhead-row limit 2^24-1");
   int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
   f->g = g;
   f->kind = kind;

@@ -145,11 +145,17 @@ struct DpView {
 // host handles
 // ---------------------------------------------------------------------------
 
-// Stream the current API call works on; DevBuf allocations are stream-ordered
-// (cudaMallocAsync from the device's default pool, whose release threshold is
-// raised once per device so freed blocks are reused instead of returned).
+// Stream the current API call works on, and the library's PRIVATE memory pool
+// of the current device: DevBuf allocations are stream-ordered
+// (cudaMallocFromPoolAsync) from a pool whose release threshold is raised so
+// freed blocks are reused across solves.  Being private, it never changes the
+// behaviour of the device's default pool that other libraries in the process
+// (PyTorch's cudaMallocAsync backend, CuPy) allocate from; remat_family_free
+// trims it back to kPoolKeepBytes.
 extern thread_local cudaStream_t tls_stream;
-void prepare_pool(int device);
+extern thread_local cudaMemPool_t tls_pool;
+constexpr size_t kPoolKeepBytes = size_t(4) << 30;
+cudaMemPool_t prepare_pool(int device);
 
 template <typename T>
 struct DevBuf {
@@ -165,7 +171,8 @@ struct DevBuf {
     if (count <= n && p) return REMAT_OK;
     release();
     size_t c = count ? count : 1;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), c * sizeof(T), tls_stream);
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), c * sizeof(T), tls_pool,
+                                            tls_stream);
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();

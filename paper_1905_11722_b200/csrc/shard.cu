@@ -33,6 +33,7 @@ struct NcclApi {
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
 };
 
@@ -51,6 +52,7 @@ static NcclApi* nccl_api(std::string* why) {
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
     api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+    api.commAbort = (decltype(api.commAbort))dlsym(h, "ncclCommAbort");
     api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
     if (!api.getUniqueId || !api.commInitRank || !api.allGather || !api.commDestroy) {
       err = "NCCL library lacks the required symbols";
@@ -69,7 +71,31 @@ struct remat_comm_s {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, device = 0;
   remat::DevBuf<unsigned char> send, recv;
+  remat::DevBuf<unsigned long long> flag;  // OR of the peers' per-level status words
 };
+
+// An NCCL call failed on this rank: abort the communicator so the peers'
+// pending collectives error out instead of waiting forever, and make the
+// handle unusable (remat_comm_free then has nothing left to destroy).
+static int comm_abort(remat_comm_s* c, NcclApi* api, ncclResult_t r, const char* what) {
+  std::string msg = std::string(what) + ": " + api->errorString(r);
+  if (c->comm) {
+    if (api->commAbort) api->commAbort(c->comm);
+    c->comm = nullptr;
+  }
+  return remat::fail(REMAT_ERR_CUDA, msg + " (communicator aborted)");
+}
+
+// Per-level status agreement: every staging block starts with a 16-byte
+// header, 0 = this rank's level is valid.  OR them into *flag on the device,
+// so the level loop never waits on the host.
+__global__ void k_status_or(const unsigned char* __restrict__ recv, long long per, int world,
+                            unsigned long long* flag) {
+  unsigned long long acc = 0;
+  for (int q = threadIdx.x; q < world; q += blockDim.x)
+    acc |= *(const unsigned long long*)(recv + per * q);
+  if (acc) atomicOr(flag, acc);
+}
 
 namespace remat {
 
@@ -199,6 +225,18 @@ static Block level_block(remat_family_s* f, int lvl, int world) {
   return Block(emax, mmax, f->cur_narrow ? (long long)sizeof(EntryN) : (long long)sizeof(EntryW));
 }
 
+// Budgets back in the caller's units, and the reference's self-check
+// (planner.py:206-210) failure surfaced as an error, as remat_solve does.
+static int finish_status(remat_plan_info* info, const int64_t* budgets, int nb) {
+  int worst = REMAT_OK;
+  for (int b = 0; b < nb; b++) {
+    info[b].budget = budgets[b];
+    if (info[b].status < 0) worst = REMAT_ERR_INTERNAL;
+  }
+  if (worst < 0) return fail(worst, "plan failed the reference self-check (planner.py:206-210)");
+  return REMAT_OK;
+}
+
 static int check_same(remat_family_s* a, remat_family_s* b) {
   if (a->F != b->F || a->g->n != b->g->n || a->slots != b->slots || a->narrow != b->narrow)
     return fail(REMAT_ERR_VALUE, "level-sharded replicas must hold the same family");
@@ -270,6 +308,7 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
                               uint64_t* chain_masks, uint64_t* cached_masks,
                               int64_t* stage_memory) {
   if (!c) return fail(REMAT_ERR_VALUE, "null communicator");
+  if (!f) return fail(REMAT_ERR_VALUE, "null family handle");
   if (nb < 1) return fail(REMAT_ERR_VALUE, "need at least one budget");
   if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
     return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
@@ -285,64 +324,112 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
     bs[b] = std::min<long long>(budgets[b], 2 * g->MV);
   }
   int rc;
+  if (!c->comm) return fail(REMAT_ERR_VALUE, "communicator was aborted by an earlier failure");
   if ((rc = ensure_foff(f)) < 0) return rc;
+  const char* fx = getenv("REMAT_SHARD_EXCHANGE");
+  const bool exchange = c->world > 1 || (fx && fx[0] == '1');
+  // staging is sized once for the widest level, so nothing is allocated
+  // inside the level loop (a rank that fails an allocation there could not
+  // join the remaining collectives)
+  const long long kHdr = 16;
+  size_t per_max = kHdr;
+  if (exchange)
+    for (int lvl = 1; lvl <= g->n; lvl++)
+      if (f->level_start[lvl + 1] > f->level_start[lvl])
+        per_max = std::max<size_t>(per_max, kHdr + (size_t)nb * level_block(f, lvl, c->world).bytes);
+  int alloc_rc = REMAT_OK;
+  if (exchange && ((alloc_rc = c->send.ensure(per_max)) >= 0))
+    if ((alloc_rc = c->recv.ensure(per_max * c->world)) >= 0) alloc_rc = c->flag.ensure(1);
   if (c->world > 1) {
-    // every rank must hold the same family and solve the same budgets: one
-    // all-gather of a small header checks it before any level is exchanged
-    const int HW = 6;
+    // every rank must hold the same family, solve the same budgets and have
+    // its staging: one all-gather of a small header checks it before any
+    // level is exchanged
+    const int HW = 7;
     long long mine[HW] = {f->F, f->slots, (long long)g->n, (long long)f->narrow, (long long)nb,
-                          (long long)objective};
+                          (long long)objective, (long long)(alloc_rc < 0)};
     for (int b = 0; b < nb; b++) mine[4] = mine[4] * 1000003LL + bs[b];
-    if ((rc = c->send.ensure(sizeof mine)) < 0 || (rc = c->recv.ensure(sizeof mine * c->world)) < 0)
-      return rc;
-    RM_CUDA(cudaMemcpyAsync(c->send.p, mine, sizeof mine, cudaMemcpyHostToDevice, g->stream));
-    ncclResult_t r = api->allGather(c->send.p, c->recv.p, sizeof mine, ncclUint8, c->comm,
-                                    g->stream);
-    if (r != ncclSuccess)
-      return fail(REMAT_ERR_CUDA, std::string("ncclAllGather: ") + api->errorString(r));
+    unsigned char *sp = nullptr, *rp = nullptr;
+    if (alloc_rc >= 0) {
+      sp = c->send.p;
+      rp = c->recv.p;
+    } else {  // still join the collective, from throw-away buffers
+      RM_CUDA(cudaMallocFromPoolAsync((void**)&sp, sizeof mine * (c->world + 1), tls_pool, g->stream));
+      rp = sp + sizeof mine;
+    }
+    RM_CUDA(cudaMemcpyAsync(sp, mine, sizeof mine, cudaMemcpyHostToDevice, g->stream));
+    ncclResult_t r = api->allGather(sp, rp, sizeof mine, ncclUint8, c->comm, g->stream);
+    if (r != ncclSuccess) return comm_abort(c, api, r, "ncclAllGather");
     std::vector<long long> all((size_t)HW * c->world);
-    RM_CUDA(cudaMemcpyAsync(all.data(), c->recv.p, sizeof mine * c->world, cudaMemcpyDeviceToHost,
+    RM_CUDA(cudaMemcpyAsync(all.data(), rp, sizeof mine * c->world, cudaMemcpyDeviceToHost,
                             g->stream));
     RM_CUDA(cudaStreamSynchronize(g->stream));
-    for (int q = 0; q < c->world; q++)
+    if (alloc_rc < 0) {
+      cudaFreeAsync(sp, g->stream);
+      return alloc_rc;
+    }
+    for (int q = 0; q < c->world; q++) {
+      if (all[(size_t)q * HW + 6])
+        return fail(REMAT_ERR_NOMEM, "level-sharded rank " + std::to_string(q) +
+                                         " could not allocate its exchange buffers");
       for (int k = 0; k < HW; k++)
         if (all[(size_t)q * HW + k] != mine[k])
           return fail(REMAT_ERR_VALUE, "level-sharded ranks disagree on the family or budgets (rank " +
                                            std::to_string(q) + ")");
+    }
+  } else if (alloc_rc < 0) {
+    return alloc_rc;
   }
   if ((rc = solve_begin(f, bs, objective)) < 0) return rc;
+  if (exchange) RM_CUDA(cudaMemsetAsync(c->flag.p, 0, 8, g->stream));
   SegList sl;
-  const char* fx = getenv("REMAT_SHARD_EXCHANGE");
-  const bool force_exchange = fx && fx[0] == '1';
+  // A local failure after this point must not strand the peers in a
+  // collective: the rank stops computing, keeps joining every level's
+  // all-gather with a non-zero status header, and all ranks fail together.
+  int local = REMAT_OK;
   for (int lvl = 1; lvl <= g->n; lvl++) {
     const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
     if (w == 0) continue;
     long long lo, hi;
     part(j0, w, c->world, c->rank, &lo, &hi);
-    if ((rc = solve_level(f, lvl, lo, hi)) < 0) return rc;
+    if (local >= 0) local = solve_level(f, lvl, lo, hi);
     // a one-rank communicator has nothing to exchange (REMAT_SHARD_EXCHANGE=1
     // still runs the all-gather: the single-GPU test of the NCCL path)
-    if (c->world == 1 && !force_exchange) continue;
+    if (!exchange) {
+      if (local < 0) return local;
+      continue;
+    }
     const Block bk = level_block(f, lvl, c->world);
-    const size_t per = (size_t)nb * bk.bytes;
-    if ((rc = c->send.ensure(per)) < 0 || (rc = c->recv.ensure(per * c->world)) < 0) return rc;
-    block_segments(f, bk, nb, lo, hi, c->send.p, true, sl);
-    if ((rc = sl.flush(g->stream)) < 0) return rc;
+    const size_t per = kHdr + (size_t)nb * bk.bytes;
+    if (local >= 0) {
+      block_segments(f, bk, nb, lo, hi, c->send.p + kHdr, true, sl);
+      local = sl.flush(g->stream);
+    }
+    cudaMemsetAsync(c->send.p, local < 0 ? 0xFF : 0, kHdr, g->stream);
     ncclResult_t r = api->allGather(c->send.p, c->recv.p, per, ncclUint8, c->comm, g->stream);
-    if (r != ncclSuccess) return fail(REMAT_ERR_CUDA, std::string("ncclAllGather: ") + api->errorString(r));
+    if (r != ncclSuccess) return comm_abort(c, api, r, "ncclAllGather");
+    k_status_or<<<1, 32, 0, g->stream>>>(c->recv.p, (long long)per, c->world, c->flag.p);
+    RM_LAUNCHED();
+    if (local < 0) continue;
     for (int q = 0; q < c->world; q++) {
       if (q == c->rank) continue;
       long long qlo, qhi;
       part(j0, w, c->world, q, &qlo, &qhi);
-      block_segments(f, bk, nb, qlo, qhi, c->recv.p + per * q, false, sl);
+      block_segments(f, bk, nb, qlo, qhi, c->recv.p + per * q + kHdr, false, sl);
     }
-    if ((rc = sl.flush(g->stream)) < 0) return rc;
+    local = sl.flush(g->stream);
+  }
+  if (local < 0) return local;
+  if (exchange) {
+    unsigned long long peer_bad = 0;
+    RM_CUDA(cudaMemcpyAsync(&peer_bad, c->flag.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    RM_CUDA(cudaStreamSynchronize(g->stream));
+    if (peer_bad)
+      return fail(REMAT_ERR_CUDA, "a peer rank failed during the level-sharded solve");
   }
   if ((rc = solve_finish(f, info, (u64*)chain_masks, (u64*)cached_masks,
                          (long long*)stage_memory)) < 0)
     return rc;
-  for (int b = 0; b < nb; b++) info[b].budget = budgets[b];
-  return REMAT_OK;
+  return finish_status(info, budgets, nb);
 }
 
 int remat_solve_level_sharded_loopback(remat_family_t* fams, int32_t world,
@@ -350,6 +437,8 @@ int remat_solve_level_sharded_loopback(remat_family_t* fams, int32_t world,
                                        remat_plan_info* info, uint64_t* chain_masks,
                                        uint64_t* cached_masks, int64_t* stage_memory) {
   if (world < 1 || !fams) return fail(REMAT_ERR_VALUE, "need at least one replica");
+  for (int r = 0; r < world; r++)
+    if (!fams[r]) return fail(REMAT_ERR_VALUE, "null family handle");
   if (nb < 1) return fail(REMAT_ERR_VALUE, "need at least one budget");
   if (objective != REMAT_MINIMIZE && objective != REMAT_MAXIMIZE)
     return fail(REMAT_ERR_VALUE, "objective must be minimize (0) or maximize (1)");
@@ -411,13 +500,12 @@ int remat_solve_level_sharded_loopback(remat_family_t* fams, int32_t world,
                          (long long*)stage_memory)) < 0)
     return rc;
   for (int b = 0; b < nb; b++) {
-    info[b].budget = budgets[b];
     if (world > 1 && (other[b].objective_value != info[b].objective_value ||
                       other[b].stats.transitions != info[b].stats.transitions ||
                       other[b].status != info[b].status))
       return fail(REMAT_ERR_INTERNAL, "level-sharded replicas disagree");
   }
-  return REMAT_OK;
+  return finish_status(info, budgets, nb);
 }
 
 }  // extern "C"

@@ -81,6 +81,9 @@ def _result(unpacked, budget, family: str, objective: str, wall: float) -> PlanR
     st = info.stats
     stats = SearchStats(st.states_visited, st.table_entries, st.transitions,
                         st.dominated_skipped, wall)
+    if info.status < 0:  # a failed self-check is an error, never "infeasible"
+        raise PlannerError(f"plan for budget {budget} failed the reference self-check "
+                           "(planner.py:206-210)")
     if info.status != 0:
         return PlanResult(False, None, None, None, budget, family, objective, stats)
     prev = 0

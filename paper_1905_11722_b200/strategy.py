@@ -58,9 +58,9 @@ def _validate(g, masks: tuple[NodeSet, ...]) -> tuple[NodeSet, ...]:
 
 
 def _device_graph(g):
-    from ._native import DeviceGraph
+    from .graph import device_graph
 
-    return DeviceGraph(g)
+    return device_graph(g)
 
 
 def make_sequence(g, chain: Iterable[NodeSet]) -> LowerSetSequence:

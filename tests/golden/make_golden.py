@@ -437,6 +437,60 @@ def bench_configs():
     return out
 
 
+def loader_corpus():
+    """graph_from_document (graph.py:185-262) on shuffled documents — node and
+    edge order permuted, input nodes, duplicate edges, default costs — and on
+    malformed documents: the reference's index order or its error message."""
+    from remat.graph import GraphError
+
+    rng = random.Random(0x10AD)
+    out = []
+    for trial in range(300):
+        n = rng.randint(1, 24)
+        nodes = []
+        for i in range(n):
+            e = {"id": f"n{i}", "memory_cost": rng.randint(1, 9)}
+            if rng.random() < 0.5:
+                e["compute_cost"] = rng.randint(0, 12)
+            if rng.random() < 0.3:
+                e["kind"] = rng.choice(["conv", "relu", "add"])
+            if rng.random() < 0.12:
+                e["is_input"] = True
+            nodes.append(e)
+        p = rng.choice([0.1, 0.3, 0.6])
+        edges = [[f"n{i}", f"n{j}"] for i in range(n) for j in range(i + 1, n) if rng.random() < p]
+        if edges and rng.random() < 0.3:
+            edges.append(list(rng.choice(edges)))  # a duplicate edge
+        rng.shuffle(nodes)
+        rng.shuffle(edges)
+        if trial % 10 == 9 and edges:  # a back edge: cycle
+            a, b = rng.choice(edges)
+            edges.append([b, a])
+        doc = {"nodes": nodes, "edges": edges}
+        try:
+            out.append({"doc": doc, "graph": graph_to_document(graph_from_document(doc))})
+        except GraphError as exc:
+            out.append({"doc": doc, "error": str(exc)})
+    bad = [
+        [], {"nodes": 3}, {"nodes": [], "edges": {}}, {"nodes": [3]}, {"nodes": [{"id": ""}]},
+        {"nodes": [{"id": 7}]}, {"nodes": [{"id": "a", "memory_cost": 1}], "edges": [["a"]]},
+        {"nodes": [{"id": "a", "memory_cost": 1}], "edges": [["a", "z"]]},
+        {"nodes": [{"id": "a", "memory_cost": 1}], "edges": [["z", "a"]]},
+        {"nodes": [{"id": "a", "memory_cost": 1, "kind": 5}]},
+        {"nodes": [{"id": "a", "memory_cost": 1, "compute_cost": -1}]},
+        {"nodes": [{"id": "a", "memory_cost": 1, "compute_cost": 1.5}]},
+        {"nodes": [{"id": "a", "memory_cost": 2**62}, {"id": "b", "memory_cost": 2**62}]},
+        {"nodes": [{"id": "a", "memory_cost": 1}], "edges": [["a", "a"]]},
+        {"nodes": [{"id": "a", "memory_cost": 1}, {"id": "a", "memory_cost": 1}], "edges": 5},
+    ]
+    for doc in bad:
+        try:
+            out.append({"doc": doc, "graph": graph_to_document(graph_from_document(doc))})
+        except GraphError as exc:
+            out.append({"doc": doc, "error": str(exc)})
+    return out
+
+
 def dump(name: str, obj) -> None:
     path = OUT / name
     path.write_text(json.dumps(obj, separators=(",", ":")) + "\n")
@@ -454,6 +508,7 @@ def main() -> None:
         "reports.json": reports,
         "named.json": lambda: named(slow),
         "cli.json": cli_corpus,
+        "loader.json": loader_corpus,
     }
     if "--xslow" in sys.argv:
         jobs = {"named_xslow.json": named_xslow}
