@@ -6,6 +6,7 @@
 // evaluate.cu / simulate.cu; there is no host compute fallback.
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -20,6 +21,14 @@ static thread_local std::string g_last_error;
 thread_local cudaStream_t tls_stream = nullptr;
 
 thread_local cudaMemPool_t tls_pool = nullptr;
+
+size_t pool_keep_bytes() {
+  static size_t keep = [] {
+    const char* e = getenv("REMAT_POOL_KEEP_GB");
+    return e ? (size_t)(atof(e) * (1ull << 30)) : kPoolKeepBytes;
+  }();
+  return keep;
+}
 
 cudaMemPool_t prepare_pool(int device) {
   static std::mutex mu;
@@ -364,7 +373,7 @@ int remat_family_free(remat_family_t f) {
   delete f;
   // return what a large family held beyond the pool's working set
   cudaStreamSynchronize(g->stream);
-  cudaMemPoolTrimTo(tls_pool, kPoolKeepBytes);
+  cudaMemPoolTrimTo(tls_pool, pool_keep_bytes());
   return REMAT_OK;
 }
 

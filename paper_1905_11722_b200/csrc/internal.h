@@ -151,10 +151,11 @@ struct DpView {
 // freed blocks are reused across solves.  Being private, it never changes the
 // behaviour of the device's default pool that other libraries in the process
 // (PyTorch's cudaMallocAsync backend, CuPy) allocate from; remat_family_free
-// trims it back to kPoolKeepBytes.
+// trims it back to pool_keep_bytes() (32 GiB of the 180 GB by default).
 extern thread_local cudaStream_t tls_stream;
 extern thread_local cudaMemPool_t tls_pool;
-constexpr size_t kPoolKeepBytes = size_t(4) << 30;
+constexpr size_t kPoolKeepBytes = size_t(32) << 30;  // REMAT_POOL_KEEP_GB overrides
+size_t pool_keep_bytes();
 cudaMemPool_t prepare_pool(int device);
 
 template <typename T>
