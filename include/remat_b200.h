@@ -131,6 +131,32 @@ REMAT_API int remat_evaluate(remat_graph_t g, int32_t k, const uint64_t *chain,
 REMAT_API int remat_simulate(remat_graph_t g, int32_t nsched, const int64_t *offsets,
                    const int32_t *ops, remat_sim_info *info, int64_t *traces);
 
+/* ---- K7: schedules on the device (schedule.py:88-254) -------------------
+ * flags: bit 0 = apply liveness_pass (149-181) to each built stream,
+ *        bit 1 = simulate (184-254) the final stream (info[], traces[]).
+ * Streams come back concatenated: stream b is ops[offsets[b] .. offsets[b+1])
+ * of int32 (kind, node) pairs; `cap` is the ops capacity in instructions. */
+
+/* build_schedule (88-117) for nplans plans: plan b's chain / segments /
+ * cached sets (LowerSetSequence fields, strategy.py:40-50) are rows
+ * [Σ_{c<b} k[c], +k[b]) of the [Σk][W] arrays.  status[b] = REMAT_OK, or
+ * REMAT_ERR_INTERNAL when the reference's assert (schedule.py:111) fails. */
+REMAT_API int remat_schedule_build(remat_graph_t g, int32_t nplans, const int32_t *k,
+                                   const uint64_t *chains, const uint64_t *segments,
+                                   const uint64_t *cached, int32_t flags, int64_t cap,
+                                   int64_t *offsets, int32_t *ops, int32_t *status,
+                                   remat_sim_info *info, int64_t *traces);
+/* vanilla_schedule (120-135); *nops = its length */
+REMAT_API int remat_schedule_vanilla(remat_graph_t g, int32_t flags, int64_t cap, int64_t *nops,
+                                     int32_t *ops, remat_sim_info *info, int64_t *traces);
+/* liveness_pass and/or simulate of caller streams (offsets/ops as
+ * remat_simulate); events[s] = Σ over stream s of the refs each instruction
+ * touches (F v: |preds|+1, B v: |preds|+2+|succs|, FREE: 1). */
+REMAT_API int remat_schedule_streams(remat_graph_t g, int32_t ns, const int64_t *offsets,
+                                     const int32_t *ops, const int64_t *events, int32_t flags,
+                                     int64_t cap, int64_t *out_offsets, int32_t *out_ops,
+                                     remat_sim_info *info, int64_t *traces);
+
 /* ---- level sharding across GPUs (no reference counterpart:
  * the reference is single-threaded) ----------------------
  * The targets of every level of an exact-DP solve are split into contiguous

@@ -102,6 +102,9 @@ def lib():
             "remat_evaluate": [_P, _I32, _P, C.POINTER(_I64), _P, C.POINTER(_I64),
                                C.POINTER(_I64), _P],
             "remat_simulate": [_P, _I32, _P, _P, _P, _P],
+            "remat_schedule_build": [_P, _I32, _P, _P, _P, _P, _I32, _I64, _P, _P, _P, _P, _P],
+            "remat_schedule_vanilla": [_P, _I32, _I64, C.POINTER(_I64), _P, _P, _P],
+            "remat_schedule_streams": [_P, _I32, _P, _P, _P, _I32, _I64, _P, _P, _P, _P],
             "remat_comm_unique_id": [_P],
             "remat_comm_create": [_P, _I32, _I32, _I32, C.POINTER(_P)],
             "remat_comm_free": [_P],
@@ -124,6 +127,7 @@ def exported_symbols() -> list[str]:
         "remat_graph_stream", "remat_family_create", "remat_family_size",
         "remat_family_masks", "remat_family_free", "remat_family_timings", "remat_solve",
         "remat_min_feasible_budget", "remat_evaluate", "remat_simulate",
+        "remat_schedule_build", "remat_schedule_vanilla", "remat_schedule_streams",
         "remat_comm_unique_id", "remat_comm_create", "remat_comm_free", "remat_level_partition",
         "remat_solve_level_sharded", "remat_solve_level_sharded_loopback",
     ]
@@ -229,22 +233,89 @@ class DeviceGraph:
         return ovh.value, [int(x) for x in stage[:k]], peak.value, ctot.value, \
             array_to_masks(cached[:k])
 
+    # -- K7 schedules (csrc/schedule.cu) -----------------------------------------
+
     def simulate(self, schedules: list[np.ndarray], want_trace: bool = True):
         offs = np.zeros(len(schedules) + 1, dtype=np.int64)
         for s, ops in enumerate(schedules):
             offs[s + 1] = offs[s] + len(ops)
-        total = int(offs[-1])
-        flat = np.zeros((max(total, 1), 2), dtype=np.int32)
-        for s, ops in enumerate(schedules):
-            if len(ops):
-                flat[offs[s]:offs[s + 1]] = ops
+        flat = np.concatenate([np.asarray(o, dtype=np.int32).reshape(-1, 2) for o in schedules]
+                              + [np.zeros((1, 2), dtype=np.int32)])
         infos = (SimInfo * len(schedules))()
-        trace = np.zeros(max(total, 1), dtype=np.int64)
+        trace = np.zeros(max(int(offs[-1]), 1), dtype=np.int64)
         with self.lock:
             check(lib().remat_simulate(_live(self.handle, "graph handle"), len(schedules),
                                        offs.ctypes.data, flat.ctypes.data, C.addressof(infos),
                                        trace.ctypes.data if want_trace else None))
         return infos, offs, trace
+
+    def build(self, seqs, flags: int):
+        """Canonical schedules of ``seqs`` (LowerSetSequence-like: chain,
+        segments, cached), + liveness (flags & 1), + simulation (flags & 2).
+        Returns (ops per plan, SimInfo per plan or [], trace per plan or [])."""
+        ks = np.array([len(q.chain) for q in seqs], dtype=np.int32)
+        chains = masks_to_array([m for q in seqs for m in q.chain], self.w)
+        segs = masks_to_array([m for q in seqs for m in q.segments], self.w)
+        cached = masks_to_array([m for q in seqs for m in q.cached], self.w)
+        nb = len(seqs)
+        cap = 6 * self.n * nb
+        offs = np.zeros(nb + 1, dtype=np.int64)
+        ops = np.zeros((max(cap, 1), 2), dtype=np.int32)
+        status = np.zeros(nb, dtype=np.int32)
+        infos = (SimInfo * nb)()
+        trace = np.zeros(max(cap, 1), dtype=np.int64) if flags & 2 else None
+        with self.lock:
+            check(lib().remat_schedule_build(
+                _live(self.handle, "graph handle"), nb, ks.ctypes.data, chains.ctypes.data,
+                segs.ctypes.data, cached.ctypes.data, flags, cap, offs.ctypes.data,
+                ops.ctypes.data, status.ctypes.data, C.addressof(infos),
+                trace.ctypes.data if trace is not None else None))
+        if (status != OK).any():
+            # the reference's own assert (schedule.py:111)
+            raise AssertionError("stage targets are not live: the sequence is inconsistent")
+        outs = [ops[offs[b]:offs[b + 1]] for b in range(nb)]
+        if not flags & 2:
+            return outs, [], []
+        return outs, list(infos), [trace[offs[b]:offs[b + 1]] for b in range(nb)]
+
+    def vanilla(self, flags: int):
+        cap = 6 * self.n
+        ops = np.zeros((cap, 2), dtype=np.int32)
+        nops = _I64()
+        info = SimInfo()
+        trace = np.zeros(cap, dtype=np.int64) if flags & 2 else None
+        with self.lock:
+            check(lib().remat_schedule_vanilla(
+                _live(self.handle, "graph handle"), flags, cap, C.byref(nops), ops.ctypes.data,
+                C.byref(info), trace.ctypes.data if trace is not None else None))
+        m = nops.value
+        return ops[:m], info, (trace[:m] if trace is not None else None)
+
+    def streams(self, schedules: list[np.ndarray], events: list[int], flags: int):
+        """liveness (flags & 1) and/or simulate (flags & 2) of encoded streams.
+        Returns (liveness outputs or [], SimInfo per stream or [], traces or [])."""
+        ns = len(schedules)
+        offs = np.zeros(ns + 1, dtype=np.int64)
+        for s, o in enumerate(schedules):
+            offs[s + 1] = offs[s] + len(o)
+        flat = np.concatenate([np.asarray(o, dtype=np.int32).reshape(-1, 2) for o in schedules]
+                              + [np.zeros((1, 2), dtype=np.int32)])
+        ev = np.asarray(events, dtype=np.int64)
+        cap = 2 * int(offs[-1]) + 1
+        out_offs = np.zeros(ns + 1, dtype=np.int64)
+        out = np.zeros((cap, 2), dtype=np.int32)
+        infos = (SimInfo * ns)()
+        trace = np.zeros(cap, dtype=np.int64) if flags & 2 else None
+        with self.lock:
+            check(lib().remat_schedule_streams(
+                _live(self.handle, "graph handle"), ns, offs.ctypes.data, flat.ctypes.data,
+                ev.ctypes.data, flags, cap, out_offs.ctypes.data, out.ctypes.data,
+                C.addressof(infos), trace.ctypes.data if trace is not None else None))
+        o = out_offs if flags & 1 else offs
+        outs = [out[out_offs[s]:out_offs[s + 1]] for s in range(ns)] if flags & 1 else []
+        if not flags & 2:
+            return outs, [], []
+        return outs, list(infos), [trace[o[s]:o[s + 1]] for s in range(ns)]
 
 
 class Comm:

@@ -207,6 +207,8 @@ static int set_device(int dev, cudaStream_t s = nullptr) {
   return REMAT_OK;
 }
 
+int graph_enter(remat_graph_s* g) { return set_device(g->device, g->stream); }
+
 }  // namespace remat
 
 using namespace remat;
@@ -280,6 +282,14 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
       hp[(size_t)v * Wp + w] = preds[(size_t)v * W + w];
       hs[(size_t)v * Wp + w] = succs[(size_t)v * W + w];
     }
+  g->indeg.assign(n, 0);
+  g->outdeg.assign(n, 0);
+  for (int v = 0; v < n; v++)
+    for (int w = 0; w < W; w++) {
+      g->indeg[v] += __builtin_popcountll(preds[(size_t)v * W + w]);
+      g->outdeg[v] += __builtin_popcountll(succs[(size_t)v * W + w]);
+    }
+  for (int v = 0; v < n; v++) g->edges += g->outdeg[v];
   g->hT.assign(compute_costs, compute_costs + n);
   g->hM.assign(memory_costs, memory_costs + n);
   g->t_uniform = std::all_of(g->hT.begin(), g->hT.end(), [&](long long t) { return t == g->hT[0]; });
@@ -300,6 +310,7 @@ int remat_graph_create(int32_t device, int32_t n, const uint64_t* preds, const u
 int remat_graph_free(remat_graph_t g) {
   if (!g) return REMAT_OK;
   set_device(g->device, g->stream);
+  free_sched_scratch(g);
   g->ev.destroy();
   cudaStream_t s = g->stream;
   delete g;
@@ -535,12 +546,22 @@ int remat_simulate(remat_graph_t g, int32_t nsched, const int64_t* offsets, cons
                    remat_sim_info* info, int64_t* traces) {
   if (!g || !offsets || !ops || !info) return fail(REMAT_ERR_VALUE, "null graph handle or argument");
   if (nsched < 1) return fail(REMAT_ERR_VALUE, "need at least one schedule");
-  int rc = set_device(g->device, g->stream);
-  if (rc < 0) return rc;
-  long long total = offsets[nsched] - offsets[0];
-  if (offsets[0] != 0 || total < 0) return fail(REMAT_ERR_VALUE, "bad schedule offsets");
-  return simulate_batch(g, nsched, (const long long*)offsets, (const int*)ops, total, info,
-                        (long long*)traces);
+  if (offsets[0] != 0) return fail(REMAT_ERR_VALUE, "bad schedule offsets");
+  // exact event counts per stream (schedule.cu inst_events): F v touches
+  // preds+1 refs, B v preds+2+succs, FREE one
+  std::vector<int64_t> events(nsched, 0);
+  for (int s = 0; s < nsched; s++) {
+    if (offsets[s + 1] < offsets[s]) return fail(REMAT_ERR_VALUE, "bad schedule offsets");
+    long long e = 0;
+    for (long long q = offsets[s]; q < offsets[s + 1]; q++) {
+      const int kind = ops[2 * q], v = ops[2 * q + 1];
+      if (v < 0 || v >= g->n || kind < 0 || kind > 3) continue;
+      e += kind == 0 ? g->indeg[v] + 1 : kind == 1 ? g->indeg[v] + 2 + g->outdeg[v] : 1;
+    }
+    events[s] = e;
+  }
+  return remat_schedule_streams(g, nsched, offsets, ops, events.data(), 2, 0, nullptr, nullptr,
+                                info, traces);
 }
 
 }  // extern "C"

@@ -205,6 +205,9 @@ struct remat_graph_s {
   remat::DevBuf<u64> cls;
   remat::DevBuf<long long> coef;
   std::vector<long long> hT, hM;
+  std::vector<int> indeg, outdeg;  // host copies: exact event counts of schedules
+  long long edges = 0;
+  void* sched = nullptr;           // K7 scratch (schedule.cu), freed with the graph
   int t_uniform = 0;  // every T_v equal: candidates of a warp collide on few row slots
   // evaluate / simulate scratch
   remat::DevBuf<u64> chain_buf, bound_buf, cached_buf;
@@ -212,8 +215,6 @@ struct remat_graph_s {
   remat::DevBuf<int> int_buf;
   remat::DevBuf<long long> ll_buf;
   remat::DevBuf<int> ops_buf;
-  remat::DevBuf<long long> off_buf, trace_buf;
-  remat::DevBuf<unsigned char> runs_buf;
   remat::Events ev;
 
   remat::GraphView view() const {
@@ -292,9 +293,10 @@ int evaluate_chains(remat_graph_s* g, int nb, const u64* chains, const int* klen
                     long long* stage_mem, u64* cached_masks, long long* results,
                     long long* terms, u64* bounds);
 
-// simulate.cu
-int simulate_batch(remat_graph_s* g, int nsched, const long long* offsets_h,
-                   const int* ops_h, long long total, remat_sim_info* info,
-                   long long* traces_h);
+// api.cu: make the graph's device / stream / pool current for this thread
+int graph_enter(remat_graph_s* g);
+
+// schedule.cu (K7)
+void free_sched_scratch(remat_graph_s* g);
 
 }  // namespace remat

@@ -22,7 +22,9 @@ from paper_1905_11722_b200 import (
     stage_memories,
     vanilla_schedule,
 )
-from paper_1905_11722_b200.graph import graph_from_document
+from paper_1905_11722_b200.graph import boundary, graph_from_document
+from paper_1905_11722_b200.schedule import encode, plan_schedules
+from paper_1905_11722_b200.strategy import LowerSetSequence
 
 pytestmark = pytest.mark.gpu
 
@@ -147,3 +149,101 @@ def test_liveness_never_worse_on_device():
         before, after = simulate_many(g, [sched, liveness_pass(g, sched)])
         assert after.peak_live_memory <= before.peak_live_memory
         assert before.peak_live_memory == peak_memory(g, seq).peak_memory
+
+
+def _enc(ops):
+    kind = {"F": 0, "B": 1, "FREE_fwd": 2, "FREE_grad": 3}
+    return [[kind[k], v] for k, v in ops]
+
+
+def _seq(g, chain):
+    prev, segs, cached, acc = 0, [], [], 0
+    for m in chain:
+        segs.append(m & ~prev)
+        acc |= boundary(g, m)
+        cached.append(acc)
+        prev = m
+    return LowerSetSequence(tuple(chain), tuple(segs), tuple(cached))
+
+
+def test_device_builders_match_reference():
+    """K7 build_schedule / vanilla_schedule / liveness_pass on the device,
+    instruction for instruction against the reference (sim_corpus.json)."""
+    for rec in golden("sim_corpus.json"):
+        g = load(rec["graph"])
+        seq = _seq(g, [h(x) for x in rec["chain"]])
+        canon, van = rec["entries"][0], rec["entries"][1]
+        sched = build_schedule(g, seq)
+        assert encode(sched).tolist() == _enc(canon["schedule"])
+        assert encode(liveness_pass(g, sched)).tolist() == _enc(canon["liveness_schedule"])
+        vs = vanilla_schedule(g)
+        assert encode(vs).tolist() == _enc(van["schedule"])
+        assert encode(liveness_pass(g, vs)).tolist() == _enc(van["liveness_schedule"])
+
+
+def test_batched_build_liveness_simulate_matches_reference():
+    """plan_schedules: many plans of one graph built, rewritten and simulated
+    in one device batch, equal to the reference's per-plan results."""
+    by_graph = {}
+    for rec in golden("sim_corpus.json"):
+        by_graph.setdefault(str(rec["graph"]), []).append(rec)
+    for recs in by_graph.values():
+        g = load(recs[0]["graph"])
+        seqs = [_seq(g, [h(x) for x in r["chain"]]) for r in recs]
+        plain, preps = plan_schedules(g, seqs, liveness=False)
+        live, lreps = plan_schedules(g, seqs, liveness=True)
+        for r, ps, pr, ls, lr in zip(recs, plain, preps, live, lreps):
+            canon = r["entries"][0]
+            assert encode(ps).tolist() == _enc(canon["schedule"])
+            assert encode(ls).tolist() == _enc(canon["liveness_schedule"])
+            _check(pr, canon["result"])
+            _check(lr, canon["liveness_result"])
+
+
+def test_simulator_matches_oracle_on_named_graphs_and_mutations():
+    """Parallel simulation against the oracle's sequential replay: canonical
+    and liveness schedules of DP plans on the named shapes, and random
+    mutations of them (dropped, duplicated and swapped instructions) that
+    fault at arbitrary points."""
+    import random
+
+    import numpy as np
+
+    from oracle import oracle as orc
+    from paper_1905_11722_b200 import Solver, named_graph
+    from paper_1905_11722_b200.schedule import decode
+
+    rng = random.Random(5)
+    for g in (named_graph("densenet161"), named_graph("pspnet"), named_graph("unet", skip_len=3)):
+        s = Solver(g, "pruned")
+        b, plan = s.min_feasible_budget("minimize")
+        s.close()
+        scheds = [build_schedule(g, plan.sequence)]
+        scheds.append(liveness_pass(g, scheds[0]))
+        scheds.append(vanilla_schedule(g))
+        for _ in range(24):
+            ops = encode(rng.choice(scheds[:3])).tolist()
+            for _ in range(rng.randint(1, 3)):
+                i = rng.randrange(len(ops))
+                op = rng.choice(["drop", "dup", "swap"])
+                if op == "drop":
+                    ops.pop(i)
+                elif op == "dup":
+                    ops.insert(i, list(ops[i]))
+                else:
+                    j = rng.randrange(len(ops))
+                    ops[i], ops[j] = ops[j], ops[i]
+            scheds.append(decode(ops))
+        for rep, sc in zip(simulate_many(g, scheds), scheds):
+            ref = orc.simulate(g, np.asarray(encode(sc)))
+            if "error" in ref:
+                assert isinstance(rep, SimulationError), ref
+                idx = int(str(rep).split()[1].rstrip(":"))
+                assert idx == ref["error"][0], (str(rep), ref)
+            else:
+                assert not isinstance(rep, Exception), rep
+                assert rep.peak_live_memory == ref["peak_live_memory"]
+                assert list(rep.trace) == ref["trace"]
+                assert rep.recompute_cost == ref["recompute_cost"]
+                assert rep.total_forward_cost == ref["total_forward_cost"]
+                assert rep.backward_count == ref["backward_count"]
