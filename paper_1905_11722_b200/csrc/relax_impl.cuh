@@ -1258,10 +1258,31 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   return REMAT_OK;
 }
 
+}  // namespace remat
+#include "relax_pm.cuh"
+namespace remat {
+
+// Wide levels of long-frontier (minimize, varied T_v) solves go to the
+// predecessor-major cluster kernel (relax_pm.cuh); REMAT_PM=0/1 forces it off/on.
+template <int W, bool NARROW>
+static bool use_pm(remat_family_s* f, long long width) {
+  static const int mode = [] {
+    const char* e = getenv("REMAT_PM");
+    return e ? atoi(e) : -1;
+  }();
+  if (!NARROW || mode == 0) return false;
+  if (mode == 1) return true;
+  return f->cur_objective == REMAT_MINIMIZE && !f->g->t_uniform && width >= 64;
+}
+
 template <int W, bool NARROW>
 int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   TileArgs ta;
   if (hi <= lo) return REMAT_OK;
+  if constexpr (NARROW) {
+    PmArgs pa;
+    if (use_pm<W, NARROW>(f, hi - lo) && plan_pm<W>(f, lvl, lo, hi, pa)) return launch_pm<W>(f, pa);
+  }
   int rc = plan_level_w<W, NARROW>(f, lvl, lo, hi, ta);
   if (rc < 0) return rc;
   relax_tile_kernel<W, NARROW>()<<<dim3((unsigned)(ta.tiles * ta.splits), (unsigned)f->cur_nb),
