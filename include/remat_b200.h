@@ -101,6 +101,14 @@ REMAT_API int remat_family_masks(remat_family_t f, int64_t start, int64_t count,
                        uint64_t *out);
 REMAT_API int remat_family_free(remat_family_t f);
 REMAT_API int remat_family_timings(remat_family_t f, remat_timings *out);
+/* Per-member figures of the last solve's budget `b` for members
+ * [start, start+count): |frontier| (SearchStats.states_visited terms), |cell|
+ * (table_entries terms), Σ|frontier_i| over comparable predecessors
+ * (transitions terms, planner.py:164) and the comparable-predecessor count.
+ * Any output may be NULL.  Diagnostics for the per-level work profile. */
+REMAT_API int remat_family_member_stats(remat_family_t f, int32_t b, int64_t start,
+                                        int64_t count, int32_t *flen, int32_t *cells,
+                                        uint64_t *trans, uint64_t *pairs);
 
 /* _plan_with_index (planner.py:192-211) for nb budgets in one batched pass.
  * Optional outputs (NULL to skip), each [nb][n+1][...]:

@@ -96,6 +96,7 @@ def lib():
             "remat_family_masks": [_P, _I64, _I64, _P],
             "remat_family_free": [_P],
             "remat_family_timings": [_P, C.POINTER(Timings)],
+            "remat_family_member_stats": [_P, _I32, _I64, _I64, _P, _P, _P, _P],
             "remat_solve": [_P, _P, _I32, _I32, _P, _P, _P, _P],
             "remat_min_feasible_budget": [_P, _I32, _I32, C.POINTER(_I64), C.POINTER(PlanInfo),
                                           _P, _P, _P, C.POINTER(_I64), C.POINTER(_I64)],
@@ -125,7 +126,8 @@ def exported_symbols() -> list[str]:
         "remat_abi_version", "remat_last_error", "remat_device_count",
         "remat_kernel_launch_count", "remat_graph_create", "remat_graph_free",
         "remat_graph_stream", "remat_family_create", "remat_family_size",
-        "remat_family_masks", "remat_family_free", "remat_family_timings", "remat_solve",
+        "remat_family_masks", "remat_family_free", "remat_family_timings",
+        "remat_family_member_stats", "remat_solve",
         "remat_min_feasible_budget", "remat_evaluate", "remat_simulate",
         "remat_schedule_build", "remat_schedule_vanilla", "remat_schedule_streams",
         "remat_comm_unique_id", "remat_comm_create", "remat_comm_free", "remat_level_partition",
@@ -403,6 +405,17 @@ class DeviceFamily:
         check(lib().remat_family_masks(_live(self.handle, "family handle"), start, count,
                                        buf.ctypes.data))
         return array_to_masks(buf[:count])
+
+    def member_stats(self, b: int = 0) -> dict:
+        """Per-member |frontier|, |cell|, Σ|frontier_i| and comparable-pair
+        count of the last solve's budget ``b`` (numpy arrays of length F)."""
+        F = self.size
+        out = {"flen": np.zeros(F, np.int32), "cells": np.zeros(F, np.int32),
+               "trans": np.zeros(F, np.uint64), "pairs": np.zeros(F, np.uint64)}
+        check(lib().remat_family_member_stats(
+            _live(self.handle, "family handle"), b, 0, F, out["flen"].ctypes.data,
+            out["cells"].ctypes.data, out["trans"].ctypes.data, out["pairs"].ctypes.data))
+        return out
 
     def timings(self) -> dict:
         t = Timings()

@@ -394,6 +394,30 @@ int remat_family_timings(remat_family_t f, remat_timings* out) {
   return REMAT_OK;
 }
 
+int remat_family_member_stats(remat_family_t f, int32_t b, int64_t start, int64_t count,
+                              int32_t* flen, int32_t* cells, uint64_t* trans, uint64_t* pairs) {
+  if (!f) return fail(REMAT_ERR_VALUE, "null family handle");
+  if (f->cur_nb < 1) return fail(REMAT_ERR_VALUE, "no solve has run on this family");
+  if (b < 0 || b >= f->cur_nb) return fail(REMAT_ERR_VALUE, "budget index out of range");
+  if (start < 0 || count < 0 || start + count > f->F)
+    return fail(REMAT_ERR_VALUE, "member range out of bounds");
+  if (count == 0) return REMAT_OK;
+  int rc = set_device(f->g->device, f->g->stream);
+  if (rc < 0) return rc;
+  cudaStream_t s = f->g->stream;
+  const size_t off = (size_t)b * f->F + start;
+  if (flen)
+    RM_CUDA(cudaMemcpyAsync(flen, f->flen.p + off, 4 * count, cudaMemcpyDeviceToHost, s));
+  if (cells)
+    RM_CUDA(cudaMemcpyAsync(cells, f->ccount.p + off, 4 * count, cudaMemcpyDeviceToHost, s));
+  if (trans)
+    RM_CUDA(cudaMemcpyAsync(trans, f->trans.p + off, 8 * count, cudaMemcpyDeviceToHost, s));
+  if (pairs)
+    RM_CUDA(cudaMemcpyAsync(pairs, f->npairs.p + off, 8 * count, cudaMemcpyDeviceToHost, s));
+  RM_CUDA(cudaStreamSynchronize(s));
+  return REMAT_OK;
+}
+
 int remat_solve(remat_family_t f, const int64_t* budgets, int32_t nb, int32_t objective,
                 remat_plan_info* info, uint64_t* chain_masks, uint64_t* cached_masks,
                 int64_t* stage_memory) {

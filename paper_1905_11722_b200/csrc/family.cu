@@ -65,95 +65,13 @@ __device__ __forceinline__ bool canonical_child(const u64 (&L)[W], const u64 (&X
   return true;
 }
 
-template <int W>
-__global__ void k_enum_count(const u64* __restrict__ rows, const u64* __restrict__ maxr,
-                             long long np, const u64* __restrict__ preds, int n,
-                             long long* __restrict__ counts) {
-  const int lane = threadIdx.x & 31;
-  const long long p = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (p >= np) return;
-  u64 L[W], X[W], cx[W];
-#pragma unroll
-  for (int w = 0; w < W; w++) {
-    L[w] = rows[p * W + w];
-    X[w] = maxr[p * W + w];
-  }
-  int cnt = 0;
-  for (int v0 = 0; v0 < n; v0 += 32) {
-    int v = v0 + lane;
-    bool ok = v < n && canonical_child<W>(L, X, v, preds, cx);
-    cnt += __popc(__ballot_sync(kFull, ok));
-  }
-  if (lane == 0) counts[p] = cnt;
-}
-
-template <int W>
-__global__ void k_enum_emit(const u64* __restrict__ rows, const u64* __restrict__ maxr,
-                            long long np, const u64* __restrict__ preds, int n,
-                            const long long* __restrict__ offs, u64* __restrict__ out_rows,
-                            u64* __restrict__ out_max) {
-  const int lane = threadIdx.x & 31;
-  const long long p = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (p >= np) return;
-  u64 L[W], X[W], cx[W];
-#pragma unroll
-  for (int w = 0; w < W; w++) {
-    L[w] = rows[p * W + w];
-    X[w] = maxr[p * W + w];
-  }
-  long long pos = offs[p];
-  for (int v0 = 0; v0 < n; v0 += 32) {
-    int v = v0 + lane;
-    bool ok = v < n && canonical_child<W>(L, X, v, preds, cx);
-    unsigned bal = __ballot_sync(kFull, ok);
-    if (ok) {
-      long long at = pos + __popc(bal & ((1u << lane) - 1));
-#pragma unroll
-      for (int w = 0; w < W; w++) {
-        out_rows[at * W + w] = L[w] | ((w == (v >> 6)) ? (1ull << (v & 63)) : 0ull);
-        out_max[at * W + w] = cx[w];
-      }
-    }
-    pos += __popc(bal);
-  }
-}
-
+// (popcount-equal) masks compared as little-endian multi-word integers
 template <int W>
 __device__ __forceinline__ bool mask_less(const u64* a, const u64* b) {
 #pragma unroll
   for (int w = W - 1; w >= 0; w--)
     if (a[w] != b[w]) return a[w] < b[w];
   return false;
-}
-
-// Rank-sort one level (all members have equal popcount, all distinct):
-// rank(i) = #{k : mask_k < mask_i}.  Tiles of 256 rows staged in shared memory.
-template <int W>
-__global__ void __launch_bounds__(256) k_rank_level(const u64* __restrict__ rows,
-                                                    const u64* __restrict__ maxr, long long N,
-                                                    u64* __restrict__ out_rows,
-                                                    u64* __restrict__ out_max) {
-  __shared__ u64 tile[256 * W];
-  const long long i = (long long)blockIdx.x * 256 + threadIdx.x;
-  u64 me[W];
-#pragma unroll
-  for (int w = 0; w < W; w++) me[w] = i < N ? rows[i * W + w] : 0ull;
-  long long rank = 0;
-  for (long long t0 = 0; t0 < N; t0 += 256) {
-    long long cnt = min(256LL, N - t0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < cnt * W; e += 256) tile[e] = rows[t0 * W + e];
-    __syncthreads();
-    if (i < N)
-      for (int k = 0; k < cnt; k++) rank += mask_less<W>(tile + k * W, me);
-  }
-  if (i < N) {
-#pragma unroll
-    for (int w = 0; w < W; w++) {
-      out_rows[rank * W + w] = me[w];
-      out_max[rank * W + w] = maxr[i * W + w];
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------

@@ -1148,7 +1148,8 @@ int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int object
     rmax = std::max(rmax, f->level_maxR[l]);
   }
   const size_t need_ctr = (size_t)2 * nb * wmax;
-  const size_t need_rows = (size_t)nb * (wmax + kMaxTJ) * rmax;
+  // (rows of the last partial tile: up to 63 past the level for k_relax_wide)
+  const size_t need_rows = (size_t)nb * (wmax + 64) * rmax;
   if (need_ctr > f->ctr_cap) {
     if ((rc = f->ctr.ensure(need_ctr)) < 0) return rc;
     f->ctr_cap = need_ctr;
@@ -1262,8 +1263,9 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
 #include "relax_pm.cuh"
 namespace remat {
 
-// Wide levels of long-frontier (minimize, varied T_v) solves go to the
-// predecessor-major cluster kernel (relax_pm.cuh); REMAT_PM=0/1 forces it off/on.
+// Wide levels of long-frontier (minimize, varied T_v) solves of a budget
+// batch go to the predecessor-major cluster kernel (relax_pm.cuh);
+// REMAT_PM=0/1 forces it off/on.
 template <int W, bool NARROW>
 static bool use_pm(remat_family_s* f, long long width) {
   static const int mode = [] {
@@ -1272,7 +1274,12 @@ static bool use_pm(remat_family_s* f, long long width) {
   }();
   if (!NARROW || mode == 0) return false;
   if (mode == 1) return true;
-  return f->cur_objective == REMAT_MINIMIZE && !f->g->t_uniform && width >= 64;
+  // measured on the B200 (tools/wd_probe.py): PSPNet 64-budget sweep relax
+  // 190 -> 154 ms; single-budget U-Net c=8 14.8 -> 49.9 ms (a batch of one
+  // budget leaves the cluster grid too small and every predecessor's entry
+  // load exposed) -- so batched sweeps only
+  return f->cur_objective == REMAT_MINIMIZE && !f->g->t_uniform && width >= 64 &&
+         f->cur_nb >= 8;
 }
 
 template <int W, bool NARROW>

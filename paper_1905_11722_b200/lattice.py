@@ -76,9 +76,9 @@ class LowerSetFamily:
 
 
 def _device_graph(g):
-    from ._native import DeviceGraph
+    from .graph import device_graph
 
-    return DeviceGraph(g)
+    return device_graph(g)
 
 
 def all_lower_sets(g, cap: int = DEFAULT_LATTICE_CAP) -> LowerSetFamily:

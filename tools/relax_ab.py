@@ -1,4 +1,4 @@
-"""A/B of the predecessor-major relaxation (REMAT_PM) on the long-frontier
+"""A/B of the relaxation variants (REMAT_PM and tuning knobs) on the long-frontier
 workloads, with a parity check of every solve against the other mode's."""
 import hashlib
 import json
