@@ -80,9 +80,14 @@ __device__ __forceinline__ bool mask_less(const u64* a, const u64* b) {
 
 // closure(v) = {v} ∪ ⋃ closure(preds(v)); preds have smaller indices, so one
 // sweep in index order suffices (graph.py:98-107).  One warp, lane q owns word q.
+// The closures are read back from shared memory, or (graphs above 1024 nodes,
+// whose n·W words exceed it) from the output rows themselves: lane q reads
+// only words it wrote.
 template <int W>
-__global__ void k_closures(const u64* __restrict__ preds, int n, u64* __restrict__ cand) {
-  extern __shared__ u64 clo[];  // [n][W]
+__global__ void k_closures(const u64* __restrict__ preds, int n, u64* __restrict__ cand,
+                           int in_smem) {
+  extern __shared__ u64 clo_sm[];  // [n][W]
+  u64* clo = in_smem ? clo_sm : cand + 2 * W;
   const int q = threadIdx.x;
   for (int v = 0; v < n; v++) {
     u64 c = (q == (v >> 6)) ? (1ull << (v & 63)) : 0ull;
@@ -95,7 +100,7 @@ __global__ void k_closures(const u64* __restrict__ preds, int n, u64* __restrict
       }
     }
     if (q < W) {
-      clo[v * W + q] = c;
+      if (in_smem) clo[v * W + q] = c;
       cand[(size_t)(v + 2) * W + q] = c;
     }
     __syncwarp();
@@ -116,15 +121,19 @@ __device__ __forceinline__ int popc_row(const u64* a) {
 }
 
 // Deduplicate + order the n+2 candidates by (popcount, mask) (from_masks).
+// Rows and flags live in shared memory, or — above 1024 nodes — stay in global
+// memory (`scratch`: 2N ints).
 template <int W>
 __global__ void __launch_bounds__(1024) k_pruned_rank(const u64* __restrict__ cand, int N,
                                                       u64* __restrict__ out_rows,
-                                                      long long* __restrict__ out_count) {
+                                                      long long* __restrict__ out_count,
+                                                      int* __restrict__ scratch) {
   extern __shared__ u64 sm[];
-  u64* rows = sm;                              // [N][W]
-  int* keep = reinterpret_cast<int*>(sm + (size_t)N * W);
+  const u64* rows = scratch ? cand : sm;  // [N][W]
+  int* keep = scratch ? scratch : reinterpret_cast<int*>(sm + (size_t)N * W);
   int* pcs = keep + N;
-  for (int e = threadIdx.x; e < N * W; e += blockDim.x) rows[e] = cand[e];
+  if (!scratch)
+    for (int e = threadIdx.x; e < N * W; e += blockDim.x) sm[e] = cand[e];
   __syncthreads();
   for (int e = threadIdx.x; e < N; e += blockDim.x) pcs[e] = popc_row<W>(rows + e * W);
   __syncthreads();
@@ -468,7 +477,9 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
                                                   long long work_cap) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ u64 tile[256 * W];
+  // comparison tile of the ranking step (48 KB static shared memory at most)
+  constexpr int kRT = W <= 16 ? 256 : 64;
+  __shared__ u64 tile[kRT * W];
   extern __shared__ u64 narrow_sm[];  // [2][ncap][2W]
   const int lane = threadIdx.x & 31;
   const long long nwarps = (long long)gridDim.x * 8;
@@ -549,13 +560,13 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
       }
     // (b) partial ranks of level k over (element tile, comparison tile) tasks
     if (k <= n) {
-      const long long nt = (N + 255) / 256;
+      const long long nt = (N + 255) / 256, ntc = (N + kRT - 1) / kRT;
       // (from the last block down: when the level is narrow the first blocks
       // carry the emission tasks, so ranking runs beside them, not after)
-      for (long long task = gridDim.x - 1 - blockIdx.x; task < nt * nt; task += gridDim.x) {
-        const long long it = task / nt, tt = task - it * nt;
-        const long long i = it * 256 + threadIdx.x, t0 = tt * 256;
-        const long long c = min(256LL, N - t0);
+      for (long long task = gridDim.x - 1 - blockIdx.x; task < nt * ntc; task += gridDim.x) {
+        const long long it = task / ntc, tt = task - it * ntc;
+        const long long i = it * 256 + threadIdx.x, t0 = tt * kRT;
+        const long long c = min((long long)kRT, N - t0);
         __syncthreads();
         for (int e = threadIdx.x; e < c * W; e += 256) {
           const long long q = e / W;
@@ -671,16 +682,24 @@ static int enumerate_pruned(remat_graph_s* g, DevBuf<u64>& fam, long long* Fout)
   if ((rc = cand.ensure((size_t)N * W)) < 0 || (rc = fam.ensure((size_t)N * W)) < 0 ||
       (rc = cnt.ensure(1)) < 0)
     return rc;
+  constexpr size_t kSm = 200 << 10;  // dynamic shared memory used at most
   size_t sm1 = sizeof(u64) * n * W;
+  const int clo_smem = sm1 <= kSm;
+  if (!clo_smem) sm1 = 0;
   RM_CUDA(cudaFuncSetAttribute(k_closures<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(sm1, 1)));
-  k_closures<W><<<1, 32, sm1, s>>>(g->preds.p, n, cand.p);
+  k_closures<W><<<1, 32, sm1, s>>>(g->preds.p, n, cand.p, clo_smem);
   RM_LAUNCHED();
   size_t sm2 = sizeof(u64) * N * W + 2 * sizeof(int) * N;
+  DevBuf<int> scratch;
+  if (sm2 > kSm) {
+    if ((rc = scratch.ensure((size_t)2 * N)) < 0) return rc;
+    sm2 = 0;
+  }
   RM_CUDA(cudaFuncSetAttribute(k_pruned_rank<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sm2));
+                               (int)std::max<size_t>(sm2, 1)));
   RM_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(long long), s));
-  k_pruned_rank<W><<<1, 1024, sm2, s>>>(cand.p, N, fam.p, cnt.p);
+  k_pruned_rank<W><<<1, 1024, sm2, s>>>(cand.p, N, fam.p, cnt.p, sm2 ? nullptr : scratch.p);
   RM_LAUNCHED();
   RM_CUDA(cudaMemcpyAsync(Fout, cnt.p, sizeof(long long), cudaMemcpyDeviceToHost, s));
   RM_CUDA(cudaStreamSynchronize(s));

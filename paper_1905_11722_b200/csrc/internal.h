@@ -29,7 +29,7 @@ typedef unsigned long long u64;
 
 namespace remat {
 
-constexpr int kMaxWords = 16;        // n <= 1024
+constexpr int kMaxWords = 32;        // n <= 2048
 constexpr int kMaxClasses = 32;      // weight classes per cost vector
 constexpr int kRelaxThreads = 256;
 constexpr int kRelaxWarps = kRelaxThreads / 32;
@@ -48,7 +48,7 @@ struct __align__(16) EntryW {  // wide: one LDG.128
 
 // Words per set, padded to an instantiated width.
 inline int padded_words(int w) {
-  static const int kW[] = {1, 2, 3, 4, 6, 8, 9, 12, 16};
+  static const int kW[] = {1, 2, 3, 4, 6, 8, 9, 12, 16, 24, 32};
   for (int x : kW)
     if (x >= w) return x;
   return -1;
@@ -66,6 +66,8 @@ void dispatch_words(int Wp, F&& f) {
     case 9: f(std::integral_constant<int, 9>{}); break;
     case 12: f(std::integral_constant<int, 12>{}); break;
     case 16: f(std::integral_constant<int, 16>{}); break;
+    case 24: f(std::integral_constant<int, 24>{}); break;
+    case 32: f(std::integral_constant<int, 32>{}); break;
     default: break;
   }
 }
