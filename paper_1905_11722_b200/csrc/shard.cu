@@ -1,21 +1,25 @@
 // shard.cu — level-sharded exact DP across GPUs.
 //
-// The targets of every level are split into contiguous rank ranges; each rank
-// relaxes its share against its full replica of the finished levels, then the
-// ranks exchange the finished level with ONE all-gather: every rank packs the
-// frontier slots, back-pointers and per-member records (|frontier|, |cell|,
-// smallest m, Σ|frontier_i|, comparable pairs) of its targets into a staging
-// block of a level-wide common size, ncclAllGather over NVLink fills every
-// rank's receive buffer, and an unpack kernel writes the other ranks' blocks
-// into the local replica.  After the last level every replica holds the whole
-// table, so reconstruction, figures and statistics run unchanged on each rank
-// and every rank returns the same plan (bit-identical to one GPU: the targets'
-// values do not depend on who computed them).
+// The targets of every heavy level are split into contiguous rank ranges;
+// each rank relaxes its share against its full replica of the finished
+// levels, then the ranks exchange the finished level IN PLACE: one NCCL group
+// of broadcasts per level, rank r the root of its own share, every rank
+// receiving straight into its replica's frontier slots, back-pointers and
+// per-member records (|frontier|, |cell|, smallest m, Σ|frontier_i|,
+// comparable pairs) — no staging copy, no pack or unpack kernel.  A level's
+// members (and their frontier slots) are contiguous in family order, so a
+// rank's share is one contiguous region per array.  Light levels (less work
+// than an exchange costs) are relaxed by every rank in full and batched into
+// the cooperative multi-level launch, exactly as on one GPU.  After the last
+// level every replica holds the whole table, so reconstruction, figures and
+// statistics run unchanged on each rank and every rank returns the same plan
+// (bit-identical to one GPU: a target's value does not depend on who computed
+// it).
 //
 // NCCL is loaded at run time (dlopen "libnccl.so.2"), so the library has no
 // link-time NCCL dependency and shares the copy torch.distributed already
 // loaded.  A loopback mode runs G replicas on ONE device with device copies in
-// place of the all-gather — the CI form of the same exchange.
+// place of the broadcasts — the CI form of the same exchange.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -32,6 +36,10 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
   const char* (*errorString)(ncclResult_t) = nullptr;
@@ -51,10 +59,14 @@ static NcclApi* nccl_api(std::string* why) {
     api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
     api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
     api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+    api.broadcast = (decltype(api.broadcast))dlsym(h, "ncclBroadcast");
+    api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+    api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
     api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
     api.commAbort = (decltype(api.commAbort))dlsym(h, "ncclCommAbort");
     api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
-    if (!api.getUniqueId || !api.commInitRank || !api.allGather || !api.commDestroy) {
+    if (!api.getUniqueId || !api.commInitRank || !api.allGather || !api.broadcast ||
+        !api.groupStart || !api.groupEnd || !api.commDestroy) {
       err = "NCCL library lacks the required symbols";
       return;
     }
@@ -70,8 +82,7 @@ static NcclApi* nccl_api(std::string* why) {
 struct remat_comm_s {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0, device = 0;
-  remat::DevBuf<unsigned char> send, recv;
-  remat::DevBuf<unsigned long long> flag;  // OR of the peers' per-level status words
+  remat::DevBuf<unsigned long long> flag;  // [world] status words: non-zero once a rank failed
 };
 
 // An NCCL call failed on this rank: abort the communicator so the peers'
@@ -84,17 +95,6 @@ static int comm_abort(remat_comm_s* c, NcclApi* api, ncclResult_t r, const char*
     c->comm = nullptr;
   }
   return remat::fail(REMAT_ERR_CUDA, msg + " (communicator aborted)");
-}
-
-// Per-level status agreement: every staging block starts with a 16-byte
-// header, 0 = this rank's level is valid.  OR them into *flag on the device,
-// so the level loop never waits on the host.
-__global__ void k_status_or(const unsigned char* __restrict__ recv, long long per, int world,
-                            unsigned long long* flag) {
-  unsigned long long acc = 0;
-  for (int q = threadIdx.x; q < world; q += blockDim.x)
-    acc |= *(const unsigned long long*)(recv + per * q);
-  if (acc) atomicOr(flag, acc);
 }
 
 namespace remat {
@@ -157,50 +157,39 @@ struct SegList {
   }
 };
 
-static inline long long al16(long long x) { return (x + 15) & ~15LL; }
-
-// Staging block of one rank for one budget: entries | parents | flen | ccount
-// | mmin | trans | npairs, each section sized for the level-wide maximum.
-struct Block {
-  long long emax, mmax, esize;
-  long long off_par, off_flen, off_cc, off_mmin, off_tr, off_np, bytes;
-  Block(long long emax_, long long mmax_, long long esize_)
-      : emax(emax_), mmax(mmax_), esize(esize_) {
-    off_par = al16(emax * esize);
-    off_flen = off_par + al16(emax * 4);
-    off_cc = off_flen + al16(mmax * 4);
-    off_mmin = off_cc + al16(mmax * 4);
-    off_tr = off_mmin + al16(mmax * 8);
-    off_np = off_tr + al16(mmax * 8);
-    bytes = off_np + al16(mmax * 8);
-  }
+// The regions one rank's share [a, b) of a level occupies in a replica, per
+// budget: frontier entries and back-pointers (slots foff[a] .. foff[b]), then
+// the five per-member records.  The same (offset, bytes) list on every rank.
+struct Region {
+  size_t off;     // byte offset inside the array
+  size_t bytes;
+  int array;      // 0 fe, 1 parent, 2 flen, 3 ccount, 4 mmin, 5 trans, 6 npairs
 };
-
-// Segments between a replica's arrays and a staging block (to_stage: pack).
-static void block_segments(remat_family_s* f, const Block& bk, int nb, long long a, long long b,
-                           unsigned char* stage, bool to_stage, SegList& sl) {
+static void share_regions(remat_family_s* f, int nb, long long a, long long b,
+                          std::vector<Region>& out) {
+  out.clear();
   const long long F = f->F;
+  const size_t es = f->cur_narrow ? sizeof(EntryN) : sizeof(EntryW);
   const long long e0 = f->h_foff[a], ne = f->h_foff[b] - f->h_foff[a], m = b - a;
   for (int bb = 0; bb < nb; bb++) {
-    unsigned char* blk = stage + (size_t)bb * bk.bytes;
-    const size_t slot0 = (size_t)bb * f->slots + e0;
-    const size_t mem0 = (size_t)bb * F + a;
-    struct {
-      void* arr;
-      long long off, bytes;
-    } parts[] = {
-        {f->fe.p + slot0 * bk.esize, 0, ne * bk.esize},
-        {f->parent.p + slot0, bk.off_par, ne * 4},
-        {f->flen.p + mem0, bk.off_flen, m * 4},
-        {f->ccount.p + mem0, bk.off_cc, m * 4},
-        {f->mmin.p + mem0, bk.off_mmin, m * 8},
-        {f->trans.p + mem0, bk.off_tr, m * 8},
-        {f->npairs.p + mem0, bk.off_np, m * 8},
-    };
-    for (auto& p : parts) {
-      if (to_stage) sl.add(p.arr, blk + p.off, p.bytes);
-      else sl.add(blk + p.off, p.arr, p.bytes);
-    }
+    const size_t slot0 = (size_t)bb * f->slots + e0, mem0 = (size_t)bb * F + a;
+    const Region r[] = {{slot0 * es, ne * es, 0}, {slot0 * 4, (size_t)ne * 4, 1},
+                        {mem0 * 4, (size_t)m * 4, 2}, {mem0 * 4, (size_t)m * 4, 3},
+                        {mem0 * 8, (size_t)m * 8, 4}, {mem0 * 8, (size_t)m * 8, 5},
+                        {mem0 * 8, (size_t)m * 8, 6}};
+    for (const Region& x : r)
+      if (x.bytes) out.push_back(x);
+  }
+}
+static unsigned char* array_base(remat_family_s* f, int array) {
+  switch (array) {
+    case 0: return f->fe.p;
+    case 1: return reinterpret_cast<unsigned char*>(f->parent.p);
+    case 2: return reinterpret_cast<unsigned char*>(f->flen.p);
+    case 3: return reinterpret_cast<unsigned char*>(f->ccount.p);
+    case 4: return reinterpret_cast<unsigned char*>(f->mmin.p);
+    case 5: return reinterpret_cast<unsigned char*>(f->trans.p);
+    default: return reinterpret_cast<unsigned char*>(f->npairs.p);
   }
 }
 
@@ -213,18 +202,6 @@ static int ensure_foff(remat_family_s* f) {
   return REMAT_OK;
 }
 
-static Block level_block(remat_family_s* f, int lvl, int world) {
-  const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
-  long long emax = 0, mmax = 0;
-  for (int r = 0; r < world; r++) {
-    long long lo, hi;
-    part(j0, w, world, r, &lo, &hi);
-    emax = std::max(emax, f->h_foff[hi] - f->h_foff[lo]);
-    mmax = std::max(mmax, hi - lo);
-  }
-  return Block(emax, mmax, f->cur_narrow ? (long long)sizeof(EntryN) : (long long)sizeof(EntryW));
-}
-
 // Budgets back in the caller's units, and the reference's self-check
 // (planner.py:206-210) failure surfaced as an error, as remat_solve does.
 static int finish_status(remat_plan_info* info, const int64_t* budgets, int nb) {
@@ -235,6 +212,33 @@ static int finish_status(remat_plan_info* info, const int64_t* budgets, int nb) 
   }
   if (worst < 0) return fail(worst, "plan failed the reference self-check (planner.py:206-210)");
   return REMAT_OK;
+}
+
+// Levels whose relaxation is cheaper than an exchange are REPLICATED: every
+// rank relaxes the whole level itself (no collective), and runs of them go
+// through the cooperative multi-level launch exactly as on one GPU (C5 has
+// 517 levels; only the wide upper ones carry enough work to split).  The
+// threshold is in (target, predecessor) subset tests per budget batch
+// (REMAT_SHARD_REPLICATE overrides it; 0 shards every level).
+static long long replicate_tests() {
+  const char* e = getenv("REMAT_SHARD_REPLICATE");  // read per solve (tests toggle it)
+  return e ? atoll(e) : (4LL << 20);
+}
+
+// Relaxes a run of replicated levels (full target ranges) on one replica.
+static int relax_run(remat_family_s* f, std::vector<int>& run) {
+  int rc = REMAT_OK;
+  if (run.size() == 1)
+    rc = solve_level(f, run[0], f->level_start[run[0]], f->level_start[run[0] + 1]);
+  else if (!run.empty())
+    rc = solve_levels(f, run);
+  run.clear();
+  return rc;
+}
+
+static inline bool replicated(remat_family_s* f, int lvl, int nb) {
+  const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
+  return w * j0 * nb <= replicate_tests();
 }
 
 static int check_same(remat_family_s* a, remat_family_s* b) {
@@ -328,49 +332,33 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
   if ((rc = ensure_foff(f)) < 0) return rc;
   const char* fx = getenv("REMAT_SHARD_EXCHANGE");
   const bool exchange = c->world > 1 || (fx && fx[0] == '1');
-  // staging is sized once for the widest level, so nothing is allocated
-  // inside the level loop (a rank that fails an allocation there could not
-  // join the remaining collectives)
-  const long long kHdr = 16;
-  size_t per_max = kHdr;
-  if (exchange)
-    for (int lvl = 1; lvl <= g->n; lvl++)
-      if (f->level_start[lvl + 1] > f->level_start[lvl])
-        per_max = std::max<size_t>(per_max, kHdr + (size_t)nb * level_block(f, lvl, c->world).bytes);
-  int alloc_rc = REMAT_OK;
-  if (exchange && ((alloc_rc = c->send.ensure(per_max)) >= 0))
-    if ((alloc_rc = c->recv.ensure(per_max * c->world)) >= 0) alloc_rc = c->flag.ensure(1);
+  // one status word per rank, allocated before the level loop (a rank that
+  // fails an allocation inside it could not join the remaining collectives)
+  int alloc_rc = exchange ? c->flag.ensure(c->world) : REMAT_OK;
   if (c->world > 1) {
     // every rank must hold the same family, solve the same budgets and have
-    // its staging: one all-gather of a small header checks it before any
+    // its status words: one all-gather of a small header checks it before any
     // level is exchanged
     const int HW = 7;
     long long mine[HW] = {f->F, f->slots, (long long)g->n, (long long)f->narrow, (long long)nb,
                           (long long)objective, (long long)(alloc_rc < 0)};
     for (int b = 0; b < nb; b++) mine[4] = mine[4] * 1000003LL + bs[b];
-    unsigned char *sp = nullptr, *rp = nullptr;
-    if (alloc_rc >= 0) {
-      sp = c->send.p;
-      rp = c->recv.p;
-    } else {  // still join the collective, from throw-away buffers
-      RM_CUDA(cudaMallocFromPoolAsync((void**)&sp, sizeof mine * (c->world + 1), tls_pool, g->stream));
-      rp = sp + sizeof mine;
-    }
+    unsigned char* sp = nullptr;
+    RM_CUDA(cudaMallocFromPoolAsync((void**)&sp, sizeof mine * (c->world + 1), tls_pool, g->stream));
+    unsigned char* rp = sp + sizeof mine;
     RM_CUDA(cudaMemcpyAsync(sp, mine, sizeof mine, cudaMemcpyHostToDevice, g->stream));
     ncclResult_t r = api->allGather(sp, rp, sizeof mine, ncclUint8, c->comm, g->stream);
     if (r != ncclSuccess) return comm_abort(c, api, r, "ncclAllGather");
     std::vector<long long> all((size_t)HW * c->world);
     RM_CUDA(cudaMemcpyAsync(all.data(), rp, sizeof mine * c->world, cudaMemcpyDeviceToHost,
                             g->stream));
+    RM_CUDA(cudaFreeAsync(sp, g->stream));
     RM_CUDA(cudaStreamSynchronize(g->stream));
-    if (alloc_rc < 0) {
-      cudaFreeAsync(sp, g->stream);
-      return alloc_rc;
-    }
+    if (alloc_rc < 0) return alloc_rc;
     for (int q = 0; q < c->world; q++) {
       if (all[(size_t)q * HW + 6])
         return fail(REMAT_ERR_NOMEM, "level-sharded rank " + std::to_string(q) +
-                                         " could not allocate its exchange buffers");
+                                         " could not allocate its status words");
       for (int k = 0; k < HW; k++)
         if (all[(size_t)q * HW + k] != mine[k])
           return fail(REMAT_ERR_VALUE, "level-sharded ranks disagree on the family or budgets (rank " +
@@ -380,51 +368,62 @@ int remat_solve_level_sharded(remat_family_t f, remat_comm_t c, const int64_t* b
     return alloc_rc;
   }
   if ((rc = solve_begin(f, bs, objective)) < 0) return rc;
-  if (exchange) RM_CUDA(cudaMemsetAsync(c->flag.p, 0, 8, g->stream));
-  SegList sl;
+  if (exchange) RM_CUDA(cudaMemsetAsync(c->flag.p, 0, 8 * c->world, g->stream));
   // A local failure after this point must not strand the peers in a
-  // collective: the rank stops computing, keeps joining every level's
-  // all-gather with a non-zero status header, and all ranks fail together.
+  // collective: the rank stops computing, raises its status word and keeps
+  // joining every level's broadcasts; all ranks fail together at the end.
   int local = REMAT_OK;
+  bool flagged = false;
+  std::vector<int> run;  // replicated levels waiting for one batched launch
+  std::vector<Region> regs;
   for (int lvl = 1; lvl <= g->n; lvl++) {
     const long long j0 = f->level_start[lvl], w = f->level_start[lvl + 1] - j0;
     if (w == 0) continue;
+    if (replicated(f, lvl, nb)) {
+      run.push_back(lvl);
+      continue;
+    }
+    if (local >= 0) local = relax_run(f, run);
+    run.clear();
     long long lo, hi;
     part(j0, w, c->world, c->rank, &lo, &hi);
     if (local >= 0) local = solve_level(f, lvl, lo, hi);
     // a one-rank communicator has nothing to exchange (REMAT_SHARD_EXCHANGE=1
-    // still runs the all-gather: the single-GPU test of the NCCL path)
+    // still runs the broadcasts: the single-GPU test of the NCCL path)
     if (!exchange) {
       if (local < 0) return local;
       continue;
     }
-    const Block bk = level_block(f, lvl, c->world);
-    const size_t per = kHdr + (size_t)nb * bk.bytes;
-    if (local >= 0) {
-      block_segments(f, bk, nb, lo, hi, c->send.p + kHdr, true, sl);
-      local = sl.flush(g->stream);
+    if (local < 0 && !flagged) {
+      cudaMemsetAsync(c->flag.p + c->rank, 0xFF, 8, g->stream);
+      flagged = true;
     }
-    cudaMemsetAsync(c->send.p, local < 0 ? 0xFF : 0, kHdr, g->stream);
-    ncclResult_t r = api->allGather(c->send.p, c->recv.p, per, ncclUint8, c->comm, g->stream);
-    if (r != ncclSuccess) return comm_abort(c, api, r, "ncclAllGather");
-    k_status_or<<<1, 32, 0, g->stream>>>(c->recv.p, (long long)per, c->world, c->flag.p);
-    RM_LAUNCHED();
-    if (local < 0) continue;
-    for (int q = 0; q < c->world; q++) {
-      if (q == c->rank) continue;
+    // the finished level, in place: rank q is the root of its own share
+    ncclResult_t r = api->groupStart();
+    for (int q = 0; q < c->world && r == ncclSuccess; q++) {
       long long qlo, qhi;
       part(j0, w, c->world, q, &qlo, &qhi);
-      block_segments(f, bk, nb, qlo, qhi, c->recv.p + per * q + kHdr, false, sl);
+      share_regions(f, nb, qlo, qhi, regs);
+      for (const Region& x : regs) {
+        unsigned char* p = array_base(f, x.array) + x.off;
+        if ((r = api->broadcast(p, p, x.bytes, ncclUint8, q, c->comm, g->stream)) != ncclSuccess)
+          break;
+      }
+      if (r == ncclSuccess)
+        r = api->broadcast(c->flag.p + q, c->flag.p + q, 8, ncclUint8, q, c->comm, g->stream);
     }
-    local = sl.flush(g->stream);
+    const ncclResult_t r2 = api->groupEnd();
+    if (r != ncclSuccess) return comm_abort(c, api, r, "ncclBroadcast");
+    if (r2 != ncclSuccess) return comm_abort(c, api, r2, "ncclGroupEnd");
   }
+  if (local >= 0) local = relax_run(f, run);
   if (local < 0) return local;
   if (exchange) {
-    unsigned long long peer_bad = 0;
-    RM_CUDA(cudaMemcpyAsync(&peer_bad, c->flag.p, 8, cudaMemcpyDeviceToHost, g->stream));
+    std::vector<unsigned long long> st(c->world);
+    RM_CUDA(cudaMemcpyAsync(st.data(), c->flag.p, 8 * c->world, cudaMemcpyDeviceToHost, g->stream));
     RM_CUDA(cudaStreamSynchronize(g->stream));
-    if (peer_bad)
-      return fail(REMAT_ERR_CUDA, "a peer rank failed during the level-sharded solve");
+    for (unsigned long long x : st)
+      if (x) return fail(REMAT_ERR_CUDA, "a peer rank failed during the level-sharded solve");
   }
   if ((rc = solve_finish(f, info, (u64*)chain_masks, (u64*)cached_masks,
                          (long long*)stage_memory)) < 0)
@@ -461,36 +460,48 @@ int remat_solve_level_sharded_loopback(remat_family_t* fams, int32_t world,
   for (int r = 0; r < world; r++)
     if ((rc = ensure_foff(fams[r])) < 0 || (rc = solve_begin(fams[r], bs, objective)) < 0)
       return rc;
-  DevBuf<unsigned char> gathered;
   SegList sl;
+  std::vector<Region> regs;
+  std::vector<int> run;
+  auto flush_run = [&]() {
+    int r2 = REMAT_OK;
+    for (int r = 0; r < world && r2 >= 0; r++) {
+      std::vector<int> copy = run;
+      r2 = relax_run(fams[r], copy);
+    }
+    run.clear();
+    return r2;
+  };
   for (int lvl = 1; lvl <= g->n; lvl++) {
     const long long j0 = f0->level_start[lvl], w = f0->level_start[lvl + 1] - j0;
     if (w == 0) continue;
+    if (replicated(f0, lvl, nb)) {
+      run.push_back(lvl);
+      continue;
+    }
+    if ((rc = flush_run()) < 0) return rc;
     for (int r = 0; r < world; r++) {
       long long lo, hi;
       part(j0, w, world, r, &lo, &hi);
       if ((rc = solve_level(fams[r], lvl, lo, hi)) < 0) return rc;
     }
     if (world == 1) continue;
-    const Block bk = level_block(f0, lvl, world);
-    const size_t per = (size_t)nb * bk.bytes;
-    if ((rc = gathered.ensure(per * world)) < 0) return rc;
-    // "all-gather": every replica packs its block straight into slot r
+    // the "broadcasts": replica r's share copied straight into every other
+    // replica's same regions
     for (int r = 0; r < world; r++) {
       long long lo, hi;
       part(j0, w, world, r, &lo, &hi);
-      block_segments(fams[r], bk, nb, lo, hi, gathered.p + per * r, true, sl);
+      share_regions(fams[r], nb, lo, hi, regs);
+      for (int q = 0; q < world; q++) {
+        if (q == r) continue;
+        for (const Region& x : regs)
+          sl.add(array_base(fams[r], x.array) + x.off, array_base(fams[q], x.array) + x.off,
+                 (long long)x.bytes);
+      }
     }
     if ((rc = sl.flush(g->stream)) < 0) return rc;
-    for (int q = 0; q < world; q++)
-      for (int r = 0; r < world; r++) {
-        if (r == q) continue;
-        long long lo, hi;
-        part(j0, w, world, r, &lo, &hi);
-        block_segments(fams[q], bk, nb, lo, hi, gathered.p + per * r, false, sl);
-      }
-    if ((rc = sl.flush(g->stream)) < 0) return rc;
   }
+  if ((rc = flush_run()) < 0) return rc;
   // every replica now holds the whole table; finish on each, report replica 0
   std::vector<remat_plan_info> other(nb);
   for (int r = world - 1; r >= 1; r--) {

@@ -77,9 +77,20 @@ def test_unique_id_reaches_every_rank():
     assert got[0] == got[1] == bytes(range(128))
 
 
+@pytest.fixture(params=["0", "default"])
+def replicate(request, monkeypatch):
+    """Shard every level (REMAT_SHARD_REPLICATE=0: every level exchanged), or
+    the default split (light levels replicated on every rank, batched)."""
+    if request.param == "default":
+        monkeypatch.delenv("REMAT_SHARD_REPLICATE", raising=False)
+    else:
+        monkeypatch.setenv("REMAT_SHARD_REPLICATE", request.param)
+    return request.param
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3, 4])
-def test_loopback_level_sharding_matches_single_gpu(world):
+def test_loopback_level_sharding_matches_single_gpu(world, replicate):
     from paper_1905_11722_b200 import Solver, named_graph
     from paper_1905_11722_b200.shard import loopback_plans
 
@@ -101,7 +112,7 @@ def test_loopback_level_sharding_matches_single_gpu(world):
 
 
 @pytest.mark.gpu
-def test_loopback_level_sharding_random_dag_matches_oracle():
+def test_loopback_level_sharding_random_dag_matches_oracle(replicate):
     from oracle import oracle as orc
     from paper_1905_11722_b200 import named_graph
     from paper_1905_11722_b200.shard import loopback_plans
