@@ -144,7 +144,7 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   a.off_tL = take(TJ * W * 8);
   a.off_tB = take(TJ * W * 8);
   a.off_tc = take(TJ * 4 * 8);
-  a.off_tcls = take(TJ * 4);
+  a.off_tcls = take(TJ * 8);  // per target: path flags, nonzero-word mask
   a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
   a.off_coef = take(cls ? 2 * K * 8 : 0);
   a.off_tacc = take(TJ * 2 * 8);
@@ -370,17 +370,41 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
     for (int t = tid; t < ntj * R; t += kThreads) rows[t] = INF;
   __syncthreads();
   const int K = cv.K;
+  // The pair terms need T and M of L_i ∩ ∂L_j, i.e. T(L_i) − T(L_i ∩ I_j)
+  // with I_j = L_j \ ∂L_j the interior.  Per target, take the cheaper mask
+  // (deep lattices of dense DAGs: the interior is EMPTY on most levels of
+  // C5, so the pair terms need no popcount at all) and the cheaper method
+  // (class popcounts over its nonzero words, or a bit loop over its nodes);
+  // the chosen mask replaces ∂L_j in tB.
+  for (int jt = tid; jt < ntj; jt += kThreads) {
+    int bc = 0, ic = 0;
+    unsigned bnz = 0, inz = 0;
+    for (int w = 0; w < W; w++) {
+      const u64 bw = tB[jt * W + w], iw = tL[jt * W + w] & ~bw;
+      bc += __popcll(bw);
+      ic += __popcll(iw);
+      bnz |= (bw != 0 ? 1u : 0u) << w;
+      inz |= (iw != 0 ? 1u : 0u) << w;
+    }
+    auto cost = [&](int bits, unsigned nz) {  // ~warp instructions per pair
+      const int cls = ta.cls ? 4 * K * __popc(nz) : INT_MAX;
+      return min(cls, 6 * bits);
+    };
+    const bool interior = cost(ic, inz) < cost(bc, bnz);
+    const int bits = interior ? ic : bc;
+    const unsigned nz = interior ? inz : bnz;
+    if (interior)
+      for (int w = 0; w < W; w++) tB[jt * W + w] = tL[jt * W + w] & ~tB[jt * W + w];
+    tcls[2 * jt] = (ta.cls && 4 * K * __popc(nz) < 6 * bits ? 1 : 0) | (interior ? 2 : 0);
+    tcls[2 * jt + 1] = (int)nz;
+  }
+  __syncthreads();
   if (ta.cls) {
     for (int e = tid; e < ntj * K * W; e += kThreads) {
       const int jt = e / (K * W), r = e - jt * K * W, c = r / W, w = r - c * W;
       bjc[e] = tB[jt * W + w] & cv.cls[c * W + w];
     }
     for (int e = tid; e < 2 * K; e += kThreads) tcoef[e] = cv.coef[e];
-  }
-  for (int jt = tid; jt < ntj; jt += kThreads) {
-    int bc = 0;
-    for (int w = 0; w < W; w++) bc += __popcll(tB[jt * W + w]);
-    tcls[jt] = ta.cls && K * W < bc;
   }
   __syncthreads();
 
@@ -409,7 +433,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   u64* tL = reinterpret_cast<u64*>(sm + ta.off_tL);         // [TJ][W]
   u64* tB = reinterpret_cast<u64*>(sm + ta.off_tB);         // [TJ][W]
   long long* tc = reinterpret_cast<long long*>(sm + ta.off_tc);  // [TJ][4]
-  int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);     // [TJ]
+  int* tcls = reinterpret_cast<int*>(sm + ta.off_tcls);     // [TJ][2]
   u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
   long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);  // [K][2]
   u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
@@ -449,19 +473,24 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   const unsigned rs_base = srow ? (unsigned)__cvta_generic_to_shared(sm + ta.off_rows) : 0u;
   auto pair_q = [&](const u64 (&Li)[W], long long ii, int jt, long long MLi, long long TLi,
                     long long mmi, Q& q) {
+    // weighted popcount of L_i ∩ (∂L_j or I_j) over the mask's nonzero words
     long long ts = 0, ms = 0;
-    if (tcls[jt]) {
+    const int fl = tcls[2 * jt];
+    const unsigned nz = (unsigned)tcls[2 * jt + 1];
+    if (fl & 1) {
       const u64* bj = bjc + (size_t)jt * K * W;
       for (int cc = 0; cc < K; cc++) {
         int pc = 0;
 #pragma unroll
-        for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[cc * W + w]);
+        for (int w = 0; w < W; w++)
+          if ((nz >> w) & 1u) pc += __popcll(Li[w] & bj[cc * W + w]);
         ts += tcoef[2 * cc] * pc;
         ms += tcoef[2 * cc + 1] * pc;
       }
-    } else {
+    } else if (nz) {
 #pragma unroll
       for (int w = 0; w < W; w++) {
+        if (!((nz >> w) & 1u)) continue;
         u64 x = Li[w] & tB[jt * W + w];
         while (x) {
           const int v = w * 64 + __ffsll((long long)x) - 1;
@@ -470,6 +499,10 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           ms += __ldg(g.M + v);
         }
       }
+    }
+    if (fl & 2) {  // interior mask: T(L_i ∩ ∂L_j) = T(L_i) − T(L_i ∩ I_j)
+      ts = TLi - ts;
+      ms = MLi - ms;
     }
     const long long fixed = 2 * (tc[jt * 4 + 0] - MLi) + tc[jt * 4 + 1];
     const long long dt = tc[jt * 4 + 2] - TLi + ts;
