@@ -578,8 +578,12 @@ def other_configs(args, world, rank, local, pk) -> list:
             ms, plans = timed_calls(lambda: budget_sweep(g, budgets, fam), world, reps)
             X = sum(p.stats.transitions for p in plans)
             par = "no golden"
-            if rec and fam == "pruned":
-                bad = [b for p, r, b in zip(plans, rec["runs"], budgets)
+            # pruned: the reference's own plans; full: the pinned oracle's
+            runs = rec["runs"] if rec and fam == "pruned" else next(
+                (r["runs"] for r in _golden("oracle_large.json")
+                 if r["name"] == "pspnet_full_sweep"), None)
+            if runs and len(runs) == len(budgets):
+                bad = [b for p, r, b in zip(plans, runs, budgets)
                        if parity(p, r["plan"]) != "bit-exact"]
                 par = "bit-exact (64 budgets)" if not bad else f"MISMATCH at budgets {bad[:4]}"
             return {"config": f"C4 PSPNet (n=384), {fam}, 64-budget sweep",

@@ -371,34 +371,38 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
   __syncthreads();
   const int K = cv.K;
   // The pair terms need T and M of L_i ∩ ∂L_j, i.e. T(L_i) − T(L_i ∩ I_j)
-  // with I_j = L_j \ ∂L_j the interior.  Per target, take the cheaper mask
-  // (deep lattices of dense DAGs: the interior is EMPTY on most levels of
-  // C5, so the pair terms need no popcount at all) and the cheaper method
-  // (class popcounts over its nonzero words, or a bit loop over its nodes);
-  // the chosen mask replaces ∂L_j in tB.
-  for (int jt = tid; jt < ntj; jt += kThreads) {
-    int bc = 0, ic = 0;
-    unsigned bnz = 0, inz = 0;
-    for (int w = 0; w < W; w++) {
-      const u64 bw = tB[jt * W + w], iw = tL[jt * W + w] & ~bw;
-      bc += __popcll(bw);
-      ic += __popcll(iw);
-      bnz |= (bw != 0 ? 1u : 0u) << w;
-      inz |= (iw != 0 ? 1u : 0u) << w;
+  // with I_j = L_j \ ∂L_j the interior.  Wide sets (W >= 4) take, per
+  // target, the cheaper mask (deep lattices of dense DAGs: the interior is
+  // EMPTY on most levels of C5, so the pair terms need no popcount at all) and
+  // visit only its nonzero words; the chosen mask replaces ∂L_j in tB.  Narrow
+  // sets keep the boundary (a bit loop over a few nodes on U-Net: the extra
+  // set-up was measured +2 % there).  Either way the cheaper method: class
+  // popcounts or a bit loop over the mask's nodes.
+  if constexpr (W >= 4) {
+    for (int jt = tid; jt < ntj; jt += kThreads) {
+      int bc = 0, ic = 0;
+      unsigned bnz = 0, inz = 0;
+      for (int w = 0; w < W; w++) {
+        const u64 bw = tB[jt * W + w], iw = tL[jt * W + w] & ~bw;
+        bc += __popcll(bw);
+        ic += __popcll(iw);
+        bnz |= (bw != 0 ? 1u : 0u) << w;
+        inz |= (iw != 0 ? 1u : 0u) << w;
+      }
+      auto cost = [&](int bits, unsigned nz) {  // ~warp instructions per pair
+        const int cls = ta.cls ? 4 * K * __popc(nz) : INT_MAX;
+        return min(cls, 6 * bits);
+      };
+      const bool interior = cost(ic, inz) < cost(bc, bnz);
+      const int bits = interior ? ic : bc;
+      const unsigned nz = interior ? inz : bnz;
+      if (interior)
+        for (int w = 0; w < W; w++) tB[jt * W + w] = tL[jt * W + w] & ~tB[jt * W + w];
+      tcls[2 * jt] = (ta.cls && 4 * K * __popc(nz) < 6 * bits ? 1 : 0) | (interior ? 2 : 0);
+      tcls[2 * jt + 1] = (int)nz;
     }
-    auto cost = [&](int bits, unsigned nz) {  // ~warp instructions per pair
-      const int cls = ta.cls ? 4 * K * __popc(nz) : INT_MAX;
-      return min(cls, 6 * bits);
-    };
-    const bool interior = cost(ic, inz) < cost(bc, bnz);
-    const int bits = interior ? ic : bc;
-    const unsigned nz = interior ? inz : bnz;
-    if (interior)
-      for (int w = 0; w < W; w++) tB[jt * W + w] = tL[jt * W + w] & ~tB[jt * W + w];
-    tcls[2 * jt] = (ta.cls && 4 * K * __popc(nz) < 6 * bits ? 1 : 0) | (interior ? 2 : 0);
-    tcls[2 * jt + 1] = (int)nz;
+    __syncthreads();
   }
-  __syncthreads();
   if (ta.cls) {
     for (int e = tid; e < ntj * K * W; e += kThreads) {
       const int jt = e / (K * W), r = e - jt * K * W, c = r / W, w = r - c * W;
@@ -406,8 +410,15 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
     }
     for (int e = tid; e < 2 * K; e += kThreads) tcoef[e] = cv.coef[e];
   }
+  if constexpr (W < 4) {
+    for (int jt = tid; jt < ntj; jt += kThreads) {
+      int bc = 0;
+      for (int w = 0; w < W; w++) bc += __popcll(tB[jt * W + w]);
+      tcls[2 * jt] = ta.cls && K * W < bc;
+      tcls[2 * jt + 1] = (1 << W) - 1;
+    }
+  }
   __syncthreads();
-
 }
 
 template <int W, bool NARROW, bool COH, bool DUAL = false>
@@ -476,21 +487,22 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     // weighted popcount of L_i ∩ (∂L_j or I_j) over the mask's nonzero words
     long long ts = 0, ms = 0;
     const int fl = tcls[2 * jt];
-    const unsigned nz = (unsigned)tcls[2 * jt + 1];
+    // (narrow sets visit every word: no per-word test)
+    const unsigned nz = W >= 4 ? (unsigned)tcls[2 * jt + 1] : (1u << W) - 1;
     if (fl & 1) {
       const u64* bj = bjc + (size_t)jt * K * W;
       for (int cc = 0; cc < K; cc++) {
         int pc = 0;
 #pragma unroll
         for (int w = 0; w < W; w++)
-          if ((nz >> w) & 1u) pc += __popcll(Li[w] & bj[cc * W + w]);
+          if (W < 4 || ((nz >> w) & 1u)) pc += __popcll(Li[w] & bj[cc * W + w]);
         ts += tcoef[2 * cc] * pc;
         ms += tcoef[2 * cc + 1] * pc;
       }
     } else if (nz) {
 #pragma unroll
       for (int w = 0; w < W; w++) {
-        if (!((nz >> w) & 1u)) continue;
+        if (W >= 4 && !((nz >> w) & 1u)) continue;
         u64 x = Li[w] & tB[jt * W + w];
         while (x) {
           const int v = w * 64 + __ffsll((long long)x) - 1;
@@ -500,7 +512,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         }
       }
     }
-    if (fl & 2) {  // interior mask: T(L_i ∩ ∂L_j) = T(L_i) − T(L_i ∩ I_j)
+    if (W >= 4 && (fl & 2)) {  // interior mask: T(L_i ∩ ∂L_j) = T(L_i) − T(L_i ∩ I_j)
       ts = TLi - ts;
       ms = MLi - ms;
     }

@@ -41,6 +41,10 @@ CASES = {
                ("dp_2mv", "mfb_min")),
     # the bench headline (BASELINE configs[1]): U-Net skip 8, exact, B = 2·M(V)
     "unet_c8": ({"name": "unet", "skip_len": 8}, ("dp_2mv",)),
+    # C4 (BASELINE configs[3]) on the FULL family: the 64-budget PSPNet sweep
+    # (budgets of bench_configs.json, whose pruned-family plans are reference
+    # outputs); 1.5e11 transitions in all
+    "pspnet_full_sweep": ({"name": "pspnet"}, ("dp_sweep",)),
 }
 
 
@@ -80,6 +84,12 @@ def main():
                 rec["runs"].append({"kind": "mfb", "family": "full", "objective": "minimize",
                                     "b_min": b_min, "plan": hexed(plan),
                                     "probes": plan["probes"]})
+            elif run == "dp_sweep":
+                sweep = json.loads((OUT.parent / "bench_configs.json").read_text())["data"]
+                budgets = next(r for r in sweep if r["name"] == "pspnet_sweep")["budgets"]
+                for b in budgets:
+                    plan = orc.dp_plan(p, b, "full", "minimize", nthreads=args.threads)
+                    rec["runs"].append({"kind": "dp", "plan": hexed(plan)})
             elif run == "dp_max_bmin":
                 # memory_centric_plan (planner.py:300-313) = the maximize DP at B_min
                 plan = orc.dp_plan(p, b_min, "full", "maximize", nthreads=args.threads)
