@@ -167,11 +167,13 @@ REMAT_API int remat_schedule_streams(remat_graph_t g, int32_t ns, const int64_t 
 
 /* ---- level sharding across GPUs (no reference counterpart:
  * the reference is single-threaded) ----------------------
- * The targets of every level of an exact-DP solve are split into contiguous
- * rank ranges; after each level the ranks all-gather the finished frontiers
- * (one ncclAllGather over NVLink).  Every rank ends with the whole table and
- * returns the same plan as remat_solve on one GPU.  NCCL is loaded at run
- * time (libnccl.so.2). */
+ * The targets of every heavy level of an exact-DP solve are split into
+ * contiguous rank ranges; after each such level the ranks exchange the
+ * finished frontiers in place (one NCCL group of per-rank broadcasts over
+ * NVLink, straight into every replica).  Light levels (fewer than
+ * REMAT_SHARD_REPLICATE subset tests, default 4 Mi) are relaxed by every rank
+ * in full.  Every rank ends with the whole table and returns the same plan as
+ * remat_solve on one GPU.  NCCL is loaded at run time (libnccl.so.2). */
 REMAT_API int remat_comm_unique_id(uint8_t *id /* [REMAT_COMM_ID_BYTES] */);
 REMAT_API int remat_comm_create(const uint8_t *id, int32_t world, int32_t rank,
                                 int32_t device, remat_comm_t *out);
@@ -188,7 +190,7 @@ REMAT_API int remat_solve_level_sharded(remat_family_t f, remat_comm_t c,
                                         uint64_t *chain_masks, uint64_t *cached_masks,
                                         int64_t *stage_memory);
 /* the same exchange with `world` replicas on ONE device (device copies in
- * place of the all-gather): the single-GPU test form of level sharding.  The
+ * place of the broadcasts): the single-GPU test form of level sharding.  The
  * replicas must be families of one graph handle. */
 REMAT_API int remat_solve_level_sharded_loopback(remat_family_t *fams, int32_t world,
                                                  const int64_t *budgets, int32_t nb,
