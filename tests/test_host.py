@@ -260,7 +260,7 @@ def test_graph_size_limits_are_reported_not_crashed():
     from paper_1905_11722_b200._native import DeviceGraph
     from paper_1905_11722_b200.graph import GraphError
 
-    with pytest.raises(ValueError, match="above 1024 nodes"):
-        DeviceGraph(_raw_graph(1025))
+    with pytest.raises(ValueError, match="above 2048 nodes"):
+        DeviceGraph(_raw_graph(2049))
     with pytest.raises(GraphError, match="below 2\\^61"):
         DeviceGraph(_raw_graph(4, mcost=1 << 60))
