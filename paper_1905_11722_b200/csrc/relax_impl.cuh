@@ -19,7 +19,9 @@ constexpr int kWarps = kThreads / 32;
 // resident CTAs of the wide-bitset relaxation kernel (register cap 64; a
 // 16-byte spill at W = 9; 3 CTAs at 80 registers measured 1 % slower)
 constexpr int kTile3MinBlocks = 4;
-constexpr int kMaxTJ = 8;    // targets per tile (one comparable bit each, <= 32)
+constexpr int kMaxTJ = 32;   // targets per tile at most (one comparable bit each)
+constexpr int kTileTJ = 8;   // targets per tile by default (REMAT_TILE_TJ)
+constexpr int kRecPerWarp = 256;  // pair-record slots per warp: lanes with records x TJ
 constexpr int kDenseLanes = 16;  // lanes with a pair for lane = predecessor constants
 constexpr int kSmallF = 4;       // frontier entries kept in registers (small-frontier path)
 
@@ -123,6 +125,7 @@ struct TileArgs {
   int probe;        // small-frontier path: probe a slot before its RED (uniform T_v)
   int ctr_stride;   // counters per budget: tiles, or the widest level when budgets run
                     // through the levels independently (k_solve_small)
+  int qlanes;       // lanes per warp with a pair-record region (>= cw; 32 up to 8 targets)
   int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_coef, off_tacc, off_pairs, off_q, off_qs, off_rows;
   int bytes;
 };
@@ -133,6 +136,7 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   TileArgs a{};
   a.TJ = TJ;
   a.R = R;
+  a.qlanes = std::max(1, std::min(32, kRecPerWarp / TJ));
   a.smem_rows = smem_rows;
   a.cls = cls;
   int o = 0;
@@ -148,8 +152,8 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
   a.off_coef = take(cls ? 2 * K * 8 : 0);
   a.off_tacc = take(TJ * 2 * 8);
-  a.off_pairs = take(kWarps * 32 * TJ * 2);
-  a.off_q = take(kWarps * 32 * TJ * (int)sizeof(typename Traits<NARROW>::Q));
+  a.off_pairs = take(kWarps * a.qlanes * TJ * 2);
+  a.off_q = take(kWarps * a.qlanes * TJ * (int)sizeof(typename Traits<NARROW>::Q));
   a.off_qs = take(kWarps * 32 * (16 + 4));
   a.off_rows = take(smem_rows ? TJ * R * (int)sizeof(Key) : 0);
   a.bytes = o;
@@ -448,8 +452,9 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   u64* bjc = reinterpret_cast<u64*>(sm + ta.off_bjc);       // [TJ][K][W]
   long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);  // [K][2]
   u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
-  unsigned short* wpairs = reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 32 * TJ;
-  Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * 32 * TJ;  // feasible pairs of a chunk
+  unsigned short* wpairs =
+      reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * ta.qlanes * TJ;
+  Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * ta.qlanes * TJ;  // feasible pairs of a chunk
   const unsigned wq_sa = (unsigned)__cvta_generic_to_shared(wq);
   PredRec* wrec = reinterpret_cast<PredRec*>(sm + ta.off_qs) + warp * 32;  // live predecessors
   int* wpc = reinterpret_cast<int*>(sm + ta.off_qs + kWarps * 32 * 16) + warp * 32;
@@ -1230,7 +1235,18 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   const long long width = hi - lo;
   const int R = (int)f->level_maxR[lvl];
   // targets per tile: as many rows as fit the per-CTA row budget, <= width
-  int TJ = (int)std::min<long long>(std::min<long long>(kMaxTJ, width),
+  // long frontiers (minimize with varied T_v) take 16 targets per tile with
+  // half-width predecessor chunks (records stay 256 per warp): every entry
+  // load feeds twice the candidates (U-Net c=8 relax 14.96 -> 14.24 ms);
+  // short frontiers keep 8 (C5 p=0.2: 151 -> 170 ms at 16).  Swept 8-32 on
+  // the B200 (tools/relax_time.py); REMAT_TILE_TJ overrides.
+  static const int tile_tj_env = [] {
+    const char* e = getenv("REMAT_TILE_TJ");
+    return e ? std::max(1, std::min(kMaxTJ, atoi(e))) : 0;
+  }();
+  const bool long_frontiers = f->cur_objective == REMAT_MINIMIZE && !g->t_uniform;
+  const int tile_tj = tile_tj_env ? tile_tj_env : (long_frontiers ? 2 * kTileTJ : kTileTJ);
+  int TJ = (int)std::min<long long>(std::min<long long>(tile_tj, width),
                                     std::max<long long>(1, kRowBudget / ((long long)R * sizeof(Key))));
   const long long nch = (j0 + 31) / 32;
   // fewer targets per tile where the level is too small to give every
@@ -1259,7 +1275,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   // narrower predecessor chunks where even one target per tile leaves the GPU
   // short of (tile, chunk) tasks (chain-like levels: one target, hundreds of
   // predecessors with long frontiers)
-  int cw = 32;
+  int cw = ta.qlanes;  // (32 up to 8 targets per tile: records are qlanes x TJ per warp)
   if (!single_cta) {
     // long frontiers (minimize, varied T_v: hundreds of entries per cell)
     // go down to one predecessor per warp, so a chain-like level's items
@@ -1284,7 +1300,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   ta.rows_pb = (int)(tiles * TJ);
   ta.tiles = (int)tiles;
   ta.ctr_stride = (int)tiles;
-  ta.cw = cw;
+  ta.cw = std::min(cw, ta.qlanes);  // records: qlanes x TJ slots per warp
   ta.probe = g->t_uniform;
   if (single_cta && f->cur_objective == REMAT_MINIMIZE) {
     // one CTA walks the level: chunks narrow enough that every warp gets some,
@@ -1292,6 +1308,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
     // minimize frontiers run to hundreds of entries (maximize frontiers hold a
     // few: wide chunks are cheaper there)
     ta.cw = (int)std::max<long long>(4, std::min<long long>(32, j0 / (2 * kWarps)));
+    ta.cw = std::min(ta.cw, ta.qlanes);
   }
   ta.ctr = f->ctr.p;  // [nb][tiles] chunk counters + [nb][tiles] done counters, all zero
   if ((size_t)2 * nb * tiles > f->ctr_cap)
