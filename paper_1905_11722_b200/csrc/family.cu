@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 
 #include "device.cuh"
@@ -267,17 +268,20 @@ __global__ void k_popcount_hist(const u64* __restrict__ rows, long long F, long 
   atomicAdd(reinterpret_cast<unsigned long long*>(hist + popc_row<W>(rows + i * W)), 1ull);
 }
 
-__global__ void k_row_len(const long long* __restrict__ TL, long long F, long long* out) {
+// frontier capacity of a member: T(L)+1 overhead values, or at most `cap`
+// cells on the sparse-row path
+__global__ void k_row_len(const long long* __restrict__ TL, long long F, long long* out,
+                          long long cap) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < F) out[i] = TL[i] + 1;
+  if (i < F) out[i] = min(TL[i] + 1, cap);
 }
 
 __global__ void k_level_max(const long long* __restrict__ TL, const long long* __restrict__ ls,
-                            long long* __restrict__ out) {
+                            long long* __restrict__ out, long long cap) {
   __shared__ long long red[32];
   const int s = blockIdx.x;
   long long lo = ls[s], hi = ls[s + 1], mx = 0;
-  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) mx = max(mx, TL[i] + 1);
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) mx = max(mx, min(TL[i] + 1, cap));
 #pragma unroll
   for (int m = 16; m > 0; m >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, m));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -753,9 +757,10 @@ static int build_family_w(remat_graph_s* g, int kind, long long cap, remat_famil
   }
   RM_CUDA(cudaMemcpyAsync(lsd.p, f->level_start.data(), sizeof(long long) * (n + 2),
                           cudaMemcpyHostToDevice, s));
-  k_level_max<<<n + 1, 256, 0, s>>>(f->TL.p, lsd.p, lmax.p);
+  const long long rcap = f->sparse ? f->fcap : LLONG_MAX;
+  k_level_max<<<n + 1, 256, 0, s>>>(f->TL.p, lsd.p, lmax.p, rcap);
   RM_LAUNCHED();
-  k_row_len<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(f->TL.p, F, tmp.p);
+  k_row_len<<<(unsigned)((F + 255) / 256), 256, 0, s>>>(f->TL.p, F, tmp.p, rcap);
   RM_LAUNCHED();
   long long slots = 0;
   if ((rc = scan_exclusive(tmp.p, f->foff.p, F, s, &slots)) < 0) return rc;
@@ -775,10 +780,24 @@ static int build_family_w(remat_graph_s* g, int kind, long long cap, remat_famil
 }
 
 int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
-  // the DP keeps a dense overhead row per member (capacity T(L)+1, 32-bit t)
-  if (g->TV + 1 > (1LL << 24))
-    return fail(REMAT_ERR_RANGE, "total compute cost T(V) = " + std::to_string(g->TV) +
-                                     " exceeds the dense overhead-row limit 2^24-1");
+  // The DP keeps a dense overhead row per member (capacity T(L)+1, 32-bit t)
+  // while T(V) < 2^24; above that (FLOP-valued compute costs) the cells of a
+  // member are keyed by their overhead value instead (relax_sparse.cuh), at
+  // most REMAT_SPARSE_CELLS (default 4096) distinct values per member.
+  f->sparse = g->TV + 1 > (1LL << 24);
+  if (const char* e = getenv("REMAT_FORCE_SPARSE"))  // test hook: the sparse path on any graph
+    if (e[0] == '1') f->sparse = 1;
+  if (f->sparse) {
+    // distinct overhead values per cell (hash capacity, transient per target)
+    // and frontier slots per member (persistent)
+    const char* e = getenv("REMAT_SPARSE_CELLS");
+    const long long h = e ? atoll(e) : (1 << 20);
+    int p = 64;
+    while (p < h && p < (1 << 22)) p <<= 1;
+    f->hcap = p;
+    const char* fr = getenv("REMAT_SPARSE_FRONTIER");
+    f->fcap = std::max<long long>(2, fr ? atoll(fr) : 4096);
+  }
   int rc = fail(REMAT_ERR_VALUE, "unsupported word count");
   f->g = g;
   f->kind = kind;
@@ -797,7 +816,7 @@ int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
                                      std::to_string(f->F) + " members");
   // 32-bit keys hold (m2 << IB) | i for every m2 <= M(V) strictly below the
   // empty-slot sentinel 0xffffffff
-  f->narrow = ((unsigned long long)(g->MV + 1) << ib) < (1ull << 32);
+  f->narrow = ((unsigned long long)(g->MV + 1) << ib) < (1ull << 32) && !f->sparse;
   if (const char* e = getenv("REMAT_FORCE_WIDE"))
     if (e[0] == '1') f->narrow = 0;
   return REMAT_OK;

@@ -40,9 +40,8 @@ struct __align__(8) EntryN {   // narrow: one LDG.64
   unsigned t;  // accumulated overhead
   unsigned m;  // cached memory
 };
-struct __align__(16) EntryW {  // wide: one LDG.128
-  unsigned t;
-  unsigned pad;
+struct __align__(16) EntryW {  // wide: one LDG.128 (64-bit t for the sparse-row path)
+  unsigned long long t;
   long long m;
 };
 
@@ -240,6 +239,12 @@ struct remat_family_s {
   std::vector<long long> level_maxR;            // [n+1]
   // DP state for up to nb_cap budgets
   int narrow = 0;                               // 32-bit row keys + 8 B entries
+  // sparse-row path (T(V) >= 2^24: a dense overhead row per member no longer
+  // fits): cells keyed by their overhead value, at most `hcap` per member
+  int sparse = 0, hcap = 0;
+  long long fcap = 0;
+  remat::DevBuf<int> sparse_err;                // 1: a cell outgrew hcap, 2: a frontier its slots
+  remat::DevBuf<u64> sparse_scratch;            // global cells when hcap exceeds shared memory
   remat::DevBuf<unsigned char> fe;
   remat::DevBuf<int> parent, flen, ccount;
   remat::DevBuf<long long> mmin, budgets, results;

@@ -1187,6 +1187,10 @@ int begin_w(remat_family_s* f, const std::vector<long long>& budgets, int object
   RM_CUDA(cudaMemsetAsync(f->npairs.p, 0, sizeof(u64) * nb * F, s));
   RM_CUDA(cudaMemsetAsync(f->flen.p, 0, sizeof(int) * nb * F, s));
   RM_CUDA(cudaMemsetAsync(f->ccount.p, 0, sizeof(int) * nb * F, s));
+  if (f->sparse) {
+    if ((rc = f->sparse_err.ensure(1)) < 0) return rc;
+    RM_CUDA(cudaMemsetAsync(f->sparse_err.p, 0, sizeof(int), s));
+  }
   k_dp_init<NARROW><<<(nb + 127) / 128, 128, 0, s>>>(f->dp_view(), F, nb);
   RM_LAUNCHED();
   // per-level scratch for the widest level: tile counters (zero) and global
@@ -1323,6 +1327,7 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
 
 }  // namespace remat
 #include "relax_pm.cuh"
+#include "relax_sparse.cuh"
 namespace remat {
 
 // Wide levels of long-frontier (minimize, varied T_v) solves of a budget
@@ -1348,6 +1353,9 @@ template <int W, bool NARROW>
 int level_w(remat_family_s* f, int lvl, long long lo, long long hi) {
   TileArgs ta;
   if (hi <= lo) return REMAT_OK;
+  if constexpr (!NARROW) {
+    if (f->sparse) return launch_sparse<W>(f, lvl, lo, hi);
+  }
   if constexpr (NARROW) {
     PmArgs pa;
     if (use_pm<W, NARROW>(f, hi - lo) && plan_pm<W>(f, lvl, lo, hi, pa)) return launch_pm<W>(f, pa);
@@ -1368,6 +1376,11 @@ template <int W, bool NARROW>
 int levels_w(remat_family_s* f, const std::vector<int>& lvls) {
   std::vector<TileArgs> tas(lvls.size());
   int maxbytes = 0, rc;
+  if (f->sparse) {  // sparse cells: one launch per level
+    for (int l : lvls)
+      if ((rc = level_w<W, NARROW>(f, l, f->level_start[l], f->level_start[l + 1])) < 0) return rc;
+    return REMAT_OK;
+  }
   static bool attr[kMaxDevices] = {};
   if (!attr[dev_slot(f->g->device)]) {
     RM_CUDA(cudaFuncSetAttribute(k_relax_levels<W, NARROW>,
@@ -1425,6 +1438,7 @@ int levels_w(remat_family_s* f, const std::vector<int>& lvls) {
 // 1 without launching when some level's rows do not fit shared memory.
 template <int W, bool NARROW>
 int small_w(remat_family_s* f) {
+  if (f->sparse) return 1;  // sparse cells: the per-level path
   const int n = f->g->n;
   std::vector<TileArgs> tas;
   int maxbytes = 0, rc;
@@ -1505,6 +1519,18 @@ int finish_w(remat_family_s* f, remat_plan_info* info, u64* chain_masks,
                             cudaMemcpyDeviceToHost, s));
   RM_CUDA(cudaEventRecord(ev.e[6], s));
   RM_CUDA(cudaStreamSynchronize(s));
+  if (f->sparse) {
+    int err = 0;
+    RM_CUDA(cudaMemcpy(&err, f->sparse_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err == 1)
+      return fail(REMAT_ERR_RANGE, "a DP cell holds more than " + std::to_string(f->hcap * 3 / 4) +
+                                       " distinct overhead values (sparse-cell capacity); raise "
+                                       "REMAT_SPARSE_CELLS");
+    if (err)
+      return fail(REMAT_ERR_RANGE, "a DP frontier holds more than " + std::to_string(f->fcap) +
+                                       " entries (sparse frontier capacity); raise "
+                                       "REMAT_SPARSE_FRONTIER");
+  }
   float relax_ms = 0, finish_ms = 0, total_ms = 0;
   cudaEventElapsedTime(&relax_ms, ev.e[3], ev.e[4]);
   cudaEventElapsedTime(&finish_ms, ev.e[4], ev.e[5]);

@@ -144,6 +144,54 @@ def dp_corpus():
     return out
 
 
+def large_costs_corpus():
+    """FLOP-valued compute costs (T_v up to 10^12, so T(V) far above 2^24:
+    the solver's sparse-cell path) with byte-like memory costs; dp_plan at
+    budgets around B_min and 2·M(V), both families and objectives, and the
+    B_min searches (planner.py:214-223, 271-297)."""
+    rng = random.Random(0xF10B5)
+    out = []
+    for gi in range(36):
+        n = rng.randint(3, 13)
+        p = 0.15 + 0.6 * rng.random()
+        nodes = []
+        for i in range(n):
+            conv = rng.random() < 0.5
+            t = rng.randint(10**9, 10**12) if conv else rng.choice([0, rng.randint(10**6, 10**9)])
+            nodes.append({"id": f"f{i}", "kind": "conv" if conv else "other", "compute_cost": t,
+                          "memory_cost": rng.choice([1, 2, 3, 4, 8, 16]) * rng.choice([1, 1024, 4096])})
+        edges = [[f"f{i}", f"f{j}"] for i in range(n) for j in range(i + 1, n) if rng.random() < p]
+        g = graph_from_document({"nodes": nodes, "edges": edges})
+        M = g.total_memory
+        bmin, _ = min_feasible_budget(g, "full")
+        cases = []
+        for b in sorted({max(0, bmin - 1), bmin, bmin + 1, (bmin + 2 * M) // 2, 2 * M}):
+            for fam in ("full", "pruned"):
+                for obj in ("minimize", "maximize"):
+                    cases.append(plan_json(dp_plan(PlanRequest(g, b, fam, obj))))
+        mfb = []
+        for fam in ("full", "pruned"):
+            for obj in ("minimize", "maximize"):
+                b, plan = min_feasible_budget(g, fam, obj)
+                mfb.append({"family": fam, "objective": obj, "b_min": b, "plan": plan_json(plan)})
+        out.append({"graph": graph_to_document(g), "cases": cases, "mfb": mfb})
+    # a named shape with FLOP-scale costs: the U-Net (skip 2), conv nodes
+    # ~10^10-10^11 and the rest ~10^9, all distinct
+    doc = ours.unet_document(2)
+    for nd in doc["nodes"]:
+        base = 10**10 if nd.get("kind") == "conv" else 10**9
+        nd["compute_cost"] = base * rng.randint(1, 9) + rng.randint(0, 10**6)
+    g = graph_from_document(doc)
+    M = g.total_memory
+    bmin, _ = min_feasible_budget(g, "full")
+    cases = [plan_json(dp_plan(PlanRequest(g, b, fam, "minimize")))
+             for b in (bmin, 2 * M) for fam in ("full", "pruned")]
+    out.append({"graph": graph_to_document(g), "cases": cases,
+                "mfb": [{"family": "full", "objective": "minimize", "b_min": bmin,
+                         "plan": plan_json(min_feasible_budget(g, "full")[1])}]})
+    return out
+
+
 def mfb_corpus():
     rng = random.Random(0x5EA4C4)
     out = []
@@ -509,6 +557,7 @@ def main() -> None:
         "named.json": lambda: named(slow),
         "cli.json": cli_corpus,
         "loader.json": loader_corpus,
+        "large_costs.json": large_costs_corpus,
     }
     if "--xslow" in sys.argv:
         jobs = {"named_xslow.json": named_xslow}
