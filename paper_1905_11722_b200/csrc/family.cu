@@ -810,10 +810,18 @@ int build_family(remat_graph_s* g, int kind, long long cap, remat_family_s* f) {
   int ib = 1;
   while ((1LL << ib) < f->F) ib++;
   f->IB = ib;
-  if (ib >= 62 || (unsigned long long)g->MV >= ((~0ull) >> ib) - 1)
-    return fail(REMAT_ERR_RANGE, "total memory cost " + std::to_string(g->MV) +
-                                     " too large for packed DP keys with a family of " +
-                                     std::to_string(f->F) + " members");
+  if (!f->sparse && (ib >= 62 || (unsigned long long)g->MV >= ((~0ull) >> ib) - 1)) {
+    // byte-valued memory costs on a big family: no packed 64-bit key holds
+    // (m << IB) | i — the sparse-cell path keeps m and i apart (its frontier
+    // slots stay the dense capacities T(L)+1 computed above)
+    f->sparse = 1;
+    f->hcap = 1 << 20;
+    if (const char* e = getenv("REMAT_SPARSE_CELLS")) {
+      int p = 64;
+      while (p < atoll(e) && p < (1 << 22)) p <<= 1;
+      f->hcap = p;
+    }
+  }
   // 32-bit keys hold (m2 << IB) | i for every m2 <= M(V) strictly below the
   // empty-slot sentinel 0xffffffff
   f->narrow = ((unsigned long long)(g->MV + 1) << ib) < (1ull << 32) && !f->sparse;

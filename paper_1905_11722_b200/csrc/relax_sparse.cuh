@@ -11,10 +11,12 @@
 //      that passes the budget test inserts its overhead t2 into a
 //      shared-memory hash set; the set is then compacted and bitonic-sorted —
 //      the member's cells in t order (|cell| of the reference, 171-174);
-//   2. relax: every candidate again, its key (m2 << IB) | i min-reduced into
-//      the row slot of its t2's rank (binary search in the sorted cells) —
-//      the same lexicographic (m2, i) minimum as the dense kernels (strict `<`
-//      in family order, planner.py:172-175).
+//   2. relax: every candidate again, min-reduced into the row slot of its
+//      t2's rank (binary search in the sorted cells): first the smallest m2,
+//      then (third pass) the smallest predecessor index i among the
+//      candidates with that m2 — the same lexicographic (m2, i) minimum as the
+//      dense kernels' packed keys (strict `<` in family order,
+//      planner.py:172-175) without their M(V)·2^IB < 2^64 bound.
 //
 // The frontier (strict prefix-min of m in t order, t descending for maximize,
 // planner.py:153-161) then comes out of the ranked row exactly as from a dense
@@ -51,10 +53,11 @@ template <int W>
 __global__ void __launch_bounds__(kThreads)
     k_relax_sparse(FamilyView fv, GraphView g, DpView dp, SpArgs sa) {
   extern __shared__ __align__(16) u64 sp_sm[];
-  u64* const base = sa.scratch ? sa.scratch + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 2 * sa.H
+  u64* const base = sa.scratch ? sa.scratch + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 3 * sa.H
                                : sp_sm;
   u64* cells = base;          // [H] hash set, then the sorted cell list
-  u64* row = base + sa.H;     // [H] ranked row keys (scratch for the sort first)
+  u64* row = base + sa.H;     // [H] ranked row: smallest m2 (scratch for the sort first)
+  unsigned* rowi = reinterpret_cast<unsigned*>(base + 2 * sa.H);  // [H] its smallest i
   __shared__ u64 sL[W], sB[W];
   __shared__ long long sc[4];
   __shared__ unsigned long long s_tr, s_np;
@@ -79,16 +82,18 @@ __global__ void __launch_bounds__(kThreads)
     s_n = 0;
     s_bad = 0;
   }
-  for (int e = tid; e < 2 * H; e += kThreads) base[e] = kSpEmpty;
+  for (int e = tid; e < 2 * H + H / 2; e += kThreads) base[e] = kSpEmpty;
   __syncthreads();
   const long long B = dp.budgets[b];
-  const int IB = dp.IB;
   const long long fbase = (long long)b * dp.slots;
   const int* flen_b = dp.flen + (size_t)b * F;
   const long long* mmin_b = dp.mmin + (size_t)b * F;
   const EntryW* fe = reinterpret_cast<const EntryW*>(dp.fe);
   int n = 0;
-  for (int pass = 0; pass < 2; pass++) {
+  // passes: 0 collect the cells, 1 the smallest m2 per cell, 2 the smallest
+  // i among its candidates with that m2 — the lexicographic (m2, i) minimum of
+  // the dense kernels' packed keys, without their M(V)·2^IB < 2^64 bound
+  for (int pass = 0; pass < 3; pass++) {
     unsigned long long tr = 0, np = 0;
     for (long long i = tid; i < sa.pend; i += kThreads) {
       u64 Li[W];
@@ -143,7 +148,9 @@ __global__ void __launch_bounds__(kThreads)
             if (cells[mid] < t2) lo = mid + 1;
             else hi = mid;
           }
-          sp_min64(row + lo, ((u64)(x.m + dm) << IB) | (u64)i);
+          const u64 m2 = (u64)(x.m + dm);
+          if (pass == 1) sp_min64(row + lo, m2);
+          else if (row[lo] == m2) atomicMin(rowi + lo, (unsigned)i);
         }
       }
     }
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kThreads)
       atomicAdd(&s_np, np);
     }
     __syncthreads();
-    if (pass == 1) break;
+    if (pass >= 1) continue;
     if (s_bad) {
       if (tid == 0) atomicExch(sa.err, 1);
       return;  // (uniform: s_bad was read after the barrier)
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(kThreads)
     auto at = [&](int s) { return mx ? n - 1 - s : s; };
     u64 lmin = kSpEmpty;
     for (int s = s0; s < s1; s++) {
-      const u64 m = row[at(s)] >> IB;
+      const u64 m = row[at(s)];
       lmin = m < lmin ? m : lmin;
     }
     const u64 incl = warp_inclusive_min(lmin);
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(kThreads)
     int nf = 0;
     u64 run = pm;
     for (int s = s0; s < s1; s++) {
-      const u64 m = row[at(s)] >> IB;
+      const u64 m = row[at(s)];
       if (m < run) {
         nf++;
         run = m;
@@ -227,18 +234,16 @@ __global__ void __launch_bounds__(kThreads)
     int* par = dp.parent + slot0;
     int pos = nf_incl - nf;
     run = pm;
-    const u64 pmask = (1ull << IB) - 1;
     for (int s = s0; s < s1; s++) {
       const int r = at(s);
-      const u64 key = row[r];
-      const u64 m = key >> IB;
+      const u64 m = row[r];
       if (m < run) {
         run = m;
         EntryW x{};
         x.t = cells[r];
         x.m = (long long)m;
         outp[pos] = x;
-        par[pos] = (int)(key & pmask);
+        par[pos] = (int)rowi[r];
         pos++;
       }
     }
@@ -256,7 +261,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 constexpr int kSpGrid = 1024;       // CTAs per budget of a sparse level launch at most
-constexpr int kSpSmemCells = 8192;  // cells held in shared memory (2 x 64 KB)
+constexpr int kSpSmemCells = 4096;  // cells held in shared memory (t, m2, i: 80 KB)
 constexpr long long kSpScratch = 4LL << 30;  // global cell scratch of one launch at most
 
 template <int W>
@@ -264,7 +269,7 @@ static int launch_sparse(remat_family_s* f, int lvl, long long lo, long long hi)
   static bool attr[kMaxDevices] = {};
   const int H = f->hcap;
   const bool smem = H <= kSpSmemCells;
-  const size_t bytes = smem ? (size_t)2 * H * sizeof(u64) : 0;
+  const size_t bytes = smem ? (size_t)(2 * H + H / 2) * sizeof(u64) : 0;
   // (at most kSpGrid CTAs in all, and global cells of 16·H bytes per CTA
   // within kSpScratch bytes)
   const long long by_mem = smem ? kSpGrid : std::max<long long>(1, kSpScratch / (16LL * H));
@@ -281,7 +286,7 @@ static int launch_sparse(remat_family_s* f, int lvl, long long lo, long long hi)
   sa.pend = f->level_start[lvl];
   sa.scratch = nullptr;
   if (!smem) {
-    int rc = f->sparse_scratch.ensure((size_t)f->cur_nb * grid * 2 * H);
+    int rc = f->sparse_scratch.ensure((size_t)f->cur_nb * grid * 3 * H);
     if (rc < 0) return rc;
     sa.scratch = f->sparse_scratch.p;
   }

@@ -175,6 +175,28 @@ def large_costs_corpus():
                 b, plan = min_feasible_budget(g, fam, obj)
                 mfb.append({"family": fam, "objective": obj, "b_min": b, "plan": plan_json(plan)})
         out.append({"graph": graph_to_document(g), "cases": cases, "mfb": mfb})
+    # byte-valued memory so large that no 64-bit key holds (m << IB) | i:
+    # M(V) ~ 2^55-2^57 on lattices of hundreds of members (small and
+    # FLOP-valued compute costs)
+    for gi in range(12):
+        n = rng.randint(9, 13)
+        p = 0.05 + 0.25 * rng.random()
+        flops = gi % 2 == 1
+        nodes = [{"id": f"h{i}", "kind": "other",
+                  "compute_cost": rng.randint(10**9, 10**11) if flops else rng.randint(0, 10),
+                  "memory_cost": rng.randint(10**15, 2 * 10**16)} for i in range(n)]
+        edges = [[f"h{i}", f"h{j}"] for i in range(n) for j in range(i + 1, n) if rng.random() < p]
+        g = graph_from_document({"nodes": nodes, "edges": edges})
+        M = g.total_memory
+        bmin, _ = min_feasible_budget(g, "full")
+        cases = []
+        for b in sorted({bmin, (bmin + 2 * M) // 2, 2 * M}):
+            for fam in ("full", "pruned"):
+                for obj in ("minimize", "maximize"):
+                    cases.append(plan_json(dp_plan(PlanRequest(g, b, fam, obj))))
+        out.append({"graph": graph_to_document(g), "cases": cases,
+                    "mfb": [{"family": "full", "objective": "minimize", "b_min": bmin,
+                             "plan": plan_json(min_feasible_budget(g, "full")[1])}]})
     # a named shape with FLOP-scale costs: the U-Net (skip 2), conv nodes
     # ~10^10-10^11 and the rest ~10^9, all distinct
     doc = ours.unet_document(2)
