@@ -18,6 +18,24 @@ g = named_graph("resnet50")  # chain-like pruned family: one predecessor per war
 print(dp_plan(PlanRequest(g, 6929, "pruned")).objective_value)
 g = named_graph("densenet161")  # chain lattice: single-block enumeration runs
 print(dp_plan(PlanRequest(g, 2 * g.total_memory, "full", "maximize")).objective_value)
+# round 2: 16-target tiles (U-Net minimize above), pm cluster kernel (>= 8 budgets),
+# every level exchanged in the loopback, the sparse-cell path (FLOP costs:
+# global cells; forced on U-Net c=2 with shared-memory cells)
+g = named_graph("unet", skip_len=2)
+s = Solver(g, "full")
+print([p.objective_value for p in s.plans(list(range(150, 150 + 16 * 20, 20)))])
+s.close()
+os.environ["REMAT_SHARD_REPLICATE"] = "0"
+print(loopback_plans(g, [2 * g.total_memory], 2)[0].objective_value)
+del os.environ["REMAT_SHARD_REPLICATE"]
+import json
+from paper_1905_11722_b200.graph import graph_from_document
+rec = json.load(open("tests/golden/large_costs.json"))["data"][5]
+g2 = graph_from_document(rec["graph"])
+print(dp_plan(PlanRequest(g2, 2 * g2.total_memory, "full")).objective_value)
+os.environ["REMAT_FORCE_SPARSE"] = "1"
+os.environ["REMAT_SPARSE_CELLS"] = "1024"
+print(dp_plan(PlanRequest(g, 2 * g.total_memory, "full", "maximize")).objective_value)
 PY
 timeout 1200 compute-sanitizer --tool memcheck --leak-check no python /tmp/san.py > gpurun_out/memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/memcheck.log
 REMAT_FORCE_WIDE=1 timeout 1200 compute-sanitizer --tool memcheck python /tmp/san.py > gpurun_out/memcheck_wide.log 2>&1; echo "rc=$?" >> gpurun_out/memcheck_wide.log
