@@ -150,6 +150,8 @@ def check(rc: int, cap: int | None = None) -> int:
     if rc == ERR_NOMEM:
         raise MemoryError(msg)
     if rc == ERR_INTERNAL:
+        if "self-check" in msg:  # the reference's own asserts (planner.py:206-210)
+            raise AssertionError(msg)
         from .planner import PlannerError
 
         raise PlannerError(msg)

@@ -81,9 +81,9 @@ def _result(unpacked, budget, family: str, objective: str, wall: float) -> PlanR
     st = info.stats
     stats = SearchStats(st.states_visited, st.table_entries, st.transitions,
                         st.dominated_skipped, wall)
-    if info.status < 0:  # a failed self-check is an error, never "infeasible"
-        raise PlannerError(f"plan for budget {budget} failed the reference self-check "
-                           "(planner.py:206-210)")
+    if info.status < 0:  # a failed self-check is the reference's assert, never "infeasible"
+        raise AssertionError(f"plan for budget {budget} failed the reference self-check "
+                             "(planner.py:206-210)")
     if info.status != 0:
         return PlanResult(False, None, None, None, budget, family, objective, stats)
     prev = 0
@@ -227,7 +227,9 @@ def dfs_exhaustive_plan(req: PlanRequest, state_cap: int = DEFAULT_DFS_STATE_CAP
     trail: list[int] = []
     # explicit stack: (cell, t, m, next successor position)
     stack = [(0, 0, 0, 0)]
-    stats.states_visited = 1
+    stats.states_visited = 1  # the root visit counts (planner.py:242-246)
+    if stats.states_visited > state_cap:
+        raise SearchCapExceeded(f"exhaustive search exceeded {state_cap} states")
     while stack:
         i, t, m, k = stack[-1]
         if i == full:
@@ -258,8 +260,9 @@ def dfs_exhaustive_plan(req: PlanRequest, state_cap: int = DEFAULT_DFS_STATE_CAP
     t_star, path = best
     seq = make_sequence(g, [masks[j] for j in path])
     ev = peak_memory(g, seq)
+    # the reference's asserts (planner.py:265-266)
     if ev.overhead != t_star or ev.peak_memory > req.budget:
-        raise PlannerError("exhaustive search produced an inconsistent plan")
+        raise AssertionError("exhaustive search produced an inconsistent plan")
     return PlanResult(True, seq, ev, t_star, req.budget, req.family, req.objective, stats)
 
 
