@@ -333,54 +333,45 @@ def named_graph(name: str, **kw) -> ComputationGraph:
 # ---------------------------------------------------------------------------
 
 
+def _components(adj: list[int], alive: int) -> int:
+    """Connected components of the undirected skeleton restricted to the node
+    set ``alive`` (bitmask flood fill: one frontier expansion per BFS layer)."""
+    count = 0
+    left = alive
+    while left:
+        seed = left & -left
+        comp = frontier = seed
+        while frontier:
+            grow = 0
+            f = frontier
+            while f:
+                low = f & -f
+                grow |= adj[low.bit_length() - 1]
+                f ^= low
+            frontier = grow & alive & ~comp
+            comp |= frontier
+        left &= ~comp
+        count += 1
+    return count
+
+
 def articulation_points(g: ComputationGraph) -> list[int]:
-    """Cut vertices of the undirected skeleton of ``g``, ascending
-    (reference benchmarks.py:136-183).  Iterative low-link DFS."""
+    """Cut vertices of the undirected skeleton of ``g``, ascending — the set
+    the reference's low-link DFS returns (benchmarks.py:136-183), computed
+    from the definition instead: v is a cut vertex iff deleting it leaves more
+    connected components than its own component contributed (an isolated v
+    is not one).  O(n) bitmask flood fills; host-only, off the hot path."""
     n = g.n
-    nbrs = []
+    adj = [g.preds[v] | g.succs[v] for v in range(n)]
+    full = (1 << n) - 1
+    base = _components(adj, full)
+    cut = []
     for v in range(n):
-        m = g.preds[v] | g.succs[v]
-        lst = []
-        while m:
-            low_bit = m & -m
-            lst.append(low_bit.bit_length() - 1)
-            m ^= low_bit
-        nbrs.append(lst)
-    order = [-1] * n
-    low = [0] * n
-    cut = set()
-    clock = 0
-    for root in range(n):
-        if order[root] >= 0:
-            continue
-        order[root] = low[root] = clock
-        clock += 1
-        kids = 0
-        stack = [(root, -1, iter(nbrs[root]))]
-        while stack:
-            v, up, it = stack[-1]
-            for w in it:
-                if w == up:
-                    continue
-                if order[w] >= 0:
-                    low[v] = min(low[v], order[w])
-                    continue
-                order[w] = low[w] = clock
-                clock += 1
-                stack.append((w, v, iter(nbrs[w])))
-                break
-            else:
-                stack.pop()
-                if stack:
-                    p = stack[-1][0]
-                    low[p] = min(low[p], low[v])
-                    if p == root:
-                        kids += 1
-                    elif low[v] >= order[p]:
-                        cut.add(p)
-        if kids > 1:
-            cut.add(root)
-    return sorted(cut)
+        if not adj[v]:
+            continue  # isolated: removing it only removes its own component
+        if _components(adj, full & ~(1 << v)) > base:
+            cut.append(v)
+    return cut
 
 
 def chen_chain(g: ComputationGraph) -> tuple[list[int], int]:

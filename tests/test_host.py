@@ -264,3 +264,21 @@ def test_graph_size_limits_are_reported_not_crashed():
         DeviceGraph(_raw_graph(2049))
     with pytest.raises(GraphError, match="below 2\\^61"):
         DeviceGraph(_raw_graph(4, mcost=1 << 60))
+
+
+def test_chen_chain_matches_reference_reports():
+    """The Chen baseline's chain and candidate count (host-only:
+    articulation points from component counts, benchmarks.py:136-211)
+    against the reference's report goldens."""
+    from paper_1905_11722_b200.benchmarks import articulation_points, chen_chain
+
+    n = 0
+    for rec in golden("reports.json"):
+        g = load(rec["graph"])
+        chain, npoints = chen_chain(g)
+        ref = rec["chen"]["plan"]
+        assert npoints == ref["stats"]["states_visited"], rec.get("spec")
+        assert articulation_points(g) == rec["chen"]["points"], rec.get("spec")
+        assert [format(m, "x") for m in chain] == ref["chain"], rec.get("spec")
+        n += 1
+    assert n >= 6
