@@ -548,21 +548,30 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   for (long long ch = (long long)(vbx - tile * splits) * kWarps + warp; ch < nch;
        ch = next_chunk(ch)) {
     worked = true;
-    // lane = predecessor i: its set and scalars in one round of loads
-    const long long i = ch * cw + lane;
+    // lane = predecessor i: its set and scalars in one round of loads.  With
+    // chunks of <= 16 predecessors (16-target tiles) the upper half-warp
+    // mirrors the lower one and tests the upper half of the tile's targets,
+    // so no lane idles in the subset tests; the halves' masks are merged.
+    const bool split = cw <= 16 && ntj > 8;  // warp-uniform
+    const int pl = split ? (lane & 15) : lane;
+    const long long i = ch * cw + pl;
     u64 Li[W];
     int fl = 0;
     long long MLi = 0, TLi = 0, mmi = 0, foffi = 0;
     unsigned mask = 0;
-    if (lane < cw && i < pred_end) {
+    if (pl < cw && i < pred_end) {
 #pragma unroll
       for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + i);
-      fl = COH ? __ldcg(flen_b + i) : flen_b[i];
-      mmi = COH ? __ldcg(mmin_b + i) : mmin_b[i];
-      MLi = __ldg(fv.ML + i);
-      TLi = __ldg(fv.TL + i);
-      foffi = __ldg(fv.foff + i);
-      for (int jt = 0; jt < ntj; jt++) {
+      if (lane == pl) {
+        fl = COH ? __ldcg(flen_b + i) : flen_b[i];
+        mmi = COH ? __ldcg(mmin_b + i) : mmin_b[i];
+        MLi = __ldg(fv.ML + i);
+        TLi = __ldg(fv.TL + i);
+        foffi = __ldg(fv.foff + i);
+      }
+      const int j0t = split && lane >= 16 ? 8 : 0;
+      const int j1t = split && lane < 16 ? 8 : ntj;
+      for (int jt = j0t; jt < j1t; jt++) {
         u64 acc = 0;
 #pragma unroll
         for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
@@ -571,6 +580,10 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     } else {
 #pragma unroll
       for (int w = 0; w < W; w++) Li[w] = 0;
+    }
+    if (split) {
+      mask |= __shfl_xor_sync(kFull, mask, 16);
+      if (lane >= 16) mask = 0;
     }
     if (!__any_sync(kFull, mask)) continue;
     // Small frontiers (every predecessor of the chunk has <= kSmallF entries,
