@@ -140,7 +140,9 @@ class Solver:
             # cost what one does); minimize rounds spread every probe over CTAs.
             # Larger families fill the GPU with fewer probes: a round of k
             # probes costs ~k solves, so the search narrows to binary as the
-            # family grows (measured on the B200: tools/probe_sweep2.py)
+            # family grows (measured on the B200: tools/probe_sweep2.py,
+            # tools/search_sweep.py: DenseNet-161 maximize 18.0 ms at 144 probes,
+            # 20.5 / 31.9 ms at 296 / 592)
             if self.dev.size <= SMALL_FAMILY:
                 probes_per_round = 144 if objective == "maximize" else 32
             elif self.dev.size <= 15_000:
