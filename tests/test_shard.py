@@ -185,3 +185,19 @@ def test_nccl_level_sharded_path_one_rank():
     p.join(timeout=120)
     assert p.exitcode == 0
     assert res == [(True, True, True)] * 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("replicate", ["0"], indirect=True)
+def test_loopback_level_sharding_sparse_cells(replicate):
+    """Level sharding over the sparse-cell path (FLOP-valued compute costs):
+    every level exchanged between 3 replicas, plans equal to the reference's."""
+    from _util import golden, load
+    from paper_1905_11722_b200.shard import loopback_plans
+
+    for rec in golden("large_costs.json")[-3:-1]:
+        g = load(rec["graph"])
+        cases = [c for c in rec["cases"] if c["family"] == "full" and c["objective"] == "minimize"]
+        got = loopback_plans(g, [c["budget"] for c in cases], 3)
+        for plan, case in zip(got, cases):
+            assert_plan_matches(plan, case, case["budget"])
