@@ -66,6 +66,15 @@ __device__ __forceinline__ bool canonical_child(const u64 (&L)[W], const u64 (&X
   return true;
 }
 
+#ifndef REMAT_RANK_TASKS
+#define REMAT_RANK_TASKS 2
+#endif
+#ifndef REMAT_RANK_MIN_TILE
+#define REMAT_RANK_MIN_TILE 4
+#endif
+constexpr long long kRankTasks = REMAT_RANK_TASKS;     // ranking tasks per block per level
+constexpr long long kRankMinTile = REMAT_RANK_MIN_TILE;  // smallest comparison tile
+
 // (popcount-equal) masks compared as little-endian multi-word integers
 template <int W>
 __device__ __forceinline__ bool mask_less(const u64* a, const u64* b) {
@@ -564,13 +573,20 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
       }
     // (b) partial ranks of level k over (element tile, comparison tile) tasks
     if (k <= n) {
-      const long long nt = (N + 255) / 256, ntc = (N + kRT - 1) / kRT;
+      // comparison tiles narrow enough for ~2 tasks per block: a level of a
+      // few hundred members would otherwise rank on a handful of blocks while
+      // the rest wait at the barrier (C5 p=0.2: ranking was 15.8 of the 17.5
+      // ms enumeration, 50 us per level on 4 of 148 blocks)
+      const long long nt = (N + 255) / 256;
+      long long C = kRT;
+      while (C > kRankMinTile && nt * ((N + C - 1) / C) < kRankTasks * (long long)gridDim.x) C >>= 1;
+      const long long ntc = (N + C - 1) / C;
       // (from the last block down: when the level is narrow the first blocks
       // carry the emission tasks, so ranking runs beside them, not after)
       for (long long task = gridDim.x - 1 - blockIdx.x; task < nt * ntc; task += gridDim.x) {
         const long long it = task / ntc, tt = task - it * ntc;
-        const long long i = it * 256 + threadIdx.x, t0 = tt * kRT;
-        const long long c = min((long long)kRT, N - t0);
+        const long long i = it * 256 + threadIdx.x, t0 = tt * C;
+        const long long c = min(C, N - t0);
         __syncthreads();
         for (int e = threadIdx.x; e < c * W; e += 256) {
           const long long q = e / W;
