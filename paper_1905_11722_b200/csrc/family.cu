@@ -478,6 +478,12 @@ __device__ __noinline__ int enum_narrow_run(const u64* __restrict__ preds, int n
 //   status[0] 1 when the lattice exceeds `cap` (LatticeTooLargeError), 2 when
 //             it exceeds the buffers' capacity `fcap` (< cap): grow and rerun;
 //   status[1] the level a narrow run hands back
+#ifdef REMAT_ENUM_TRACE
+__device__ unsigned long long g_enum_trace[600 * 148 * 4];
+extern "C" __attribute__((visibility("default"))) int remat_debug_enum_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_enum_trace, sizeof(g_enum_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 template <int W>
 __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds, int n,
                                                   long long cap, long long fcap,
@@ -536,6 +542,16 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
     u64* nxt = U + (size_t)((k + 1) % 3) * ucap * 2 * W;
     unsigned* rk = rank + (size_t)(k % 3) * ucap;
     const long long room = min(min(cap, fcap) - base - N, ucap);  // children that fit
+#ifdef REMAT_ENUM_TRACE  // per-level phase timestamps (tools/enum_trace.py)
+    auto stamp = [&](int ph) {
+      if (threadIdx.x == 0 && k < 600) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_enum_trace[((size_t)k * 148 + (blockIdx.x % 148)) * 4 + ph] = t;
+      }
+    };
+    stamp(0);
+#endif
     // (c) scatter level k-1, leaving its rank slot zeroed for level k+2
     for (long long i = gt; i < prevN; i += nthreads) {
       const long long at = prev_base + rkp[i];
@@ -543,6 +559,9 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
 #pragma unroll
       for (int w = 0; w < W; w++) fam[at * W + w] = prv[i * 2 * W + w];
     }
+#ifdef REMAT_ENUM_TRACE
+    stamp(1);
+#endif
     // (a) canonical children of level k
     if (k < n)
       for (long long task = gw; task < N * nch; task += nwarps) {
@@ -571,6 +590,9 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
           }
         }
       }
+#ifdef REMAT_ENUM_TRACE
+    stamp(2);
+#endif
     // (b) partial ranks of level k over (element tile, comparison tile) tasks
     if (k <= n) {
       // comparison tiles narrow enough for ~2 tasks per block: a level of a
@@ -606,6 +628,10 @@ __global__ void __launch_bounds__(256) k_enum_all(const u64* __restrict__ preds,
     prev_base = base;
     prevN = k <= n ? N : 0;
     base += N;
+#ifdef REMAT_ENUM_TRACE
+    __syncthreads();
+    stamp(3);
+#endif
     grid.sync();
     k++;
   }

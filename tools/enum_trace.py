@@ -1,3 +1,10 @@
+"""Per-level phase times of the enumeration kernel (K1) on the C5 lattices:
+scatter / emit / rank per level (slowest block) and the barrier gap, from
+globaltimer stamps of a REMAT_ENUM_TRACE build:
+
+  make -C paper_1905_11722_b200/csrc OUT=$PWD/build_trace/libremat_b200.so \
+       OBJDIR=/tmp/obj_trace EXTRA=-DREMAT_ENUM_TRACE
+  python tools/enum_trace.py"""
 import ctypes as C, os, sys, json
 import numpy as np
 sys.path.insert(0, "/root/repo")
