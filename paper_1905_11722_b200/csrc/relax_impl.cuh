@@ -968,6 +968,10 @@ __global__ void __launch_bounds__(kThreads)
 // publishes the level (its tiles were finalized by their last CTA) before the
 // next one starts.  Removes the launch + ramp of each of the hundreds of
 // narrow levels of deep lattices (C5: 516 levels).
+#ifdef REMAT_RELAX_TRACE
+__device__ unsigned long long g_relax_trace[600 * 296 * 4];
+__device__ int g_relax_trace_meta[600 * 4];
+#endif
 template <int W, bool NARROW>
 __global__ void __launch_bounds__(kThreads)
     k_relax_levels(FamilyView fv, GraphView g, ClassView cv, DpView dp,
@@ -986,11 +990,24 @@ __global__ void __launch_bounds__(kThreads)
   for (int l = 0; l < nlev; l++) {
     const TileArgs ta = levels[l];
     const int per = ta.tiles * ta.splits;
+#ifdef REMAT_RELAX_TRACE
+    auto stamp = [&](int ph) {
+      if (threadIdx.x == 0 && l < 600 && blockIdx.x < 296) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_relax_trace[((size_t)l * 296 + blockIdx.x) * 4 + ph] = t;
+      }
+    };
+    stamp(0);
+#endif
     for (int v = blockIdx.x; v < per * nb; v += gridDim.x) {
       relax_body<W, NARROW, true>(fv, g, cv, dp, ta, v % per, v / per, nb, sm,
                                   pre && v == (int)blockIdx.x);
       __syncthreads();
     }
+#ifdef REMAT_RELAX_TRACE
+    stamp(1);
+#endif
     // split barrier: arrive, set up the next level's first tile, then wait
     auto token = grid.barrier_arrive();
     pre = false;
@@ -1308,6 +1325,9 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   if (max_vctas > 0) splits = max_vctas / (tiles * nb);  // persistent: one round per block
   if (single_cta) splits = 1;
   // (rounded up: every chunk of a narrow level is some warp's static first one)
+  // (fewer splits — 2-16 chunks per warp at least — measured slower on every
+  // config, tools/c5_small.py: the chunks' own latency, not the fold, bounds a
+  // narrow level; tools/relax_trace.py)
   splits = std::max(1LL, std::min(splits, (nchw + kWarps - 1) / kWarps));
   ta.jbase = lo;
   ta.pend = j0;

@@ -5,3 +5,11 @@
 namespace remat {
 REMAT_INSTANTIATE_RELAX(9)
 }  // namespace remat
+
+#ifdef REMAT_RELAX_TRACE
+namespace remat {
+extern "C" __attribute__((visibility("default"))) int remat_debug_relax_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_relax_trace, sizeof(g_relax_trace)) == cudaSuccess ? 0 : -1;
+}
+}  // namespace remat
+#endif
