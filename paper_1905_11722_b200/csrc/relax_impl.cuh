@@ -477,7 +477,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   const int cw = ta.cw;  // predecessors per chunk (32; fewer spreads narrow levels over warps)
   const long long nch = (pred_end + cw - 1) / cw;
   unsigned* ctr = ta.ctr + (size_t)b * ta.ctr_stride + tile;
-  u64 my_trans = 0;  // lane jt accumulates target jt of the tile
+  u64 my_trans = 0;  // lane = predecessor: its Σ|frontier| over comparable tile targets
   u64 my_pairs = 0;
   bool worked = false;
 
@@ -494,7 +494,20 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     const int fl = tcls[2 * jt];
     // (narrow sets visit every word: no per-word test)
     const unsigned nz = W >= 4 ? (unsigned)tcls[2 * jt + 1] : (1u << W) - 1;
-    if (fl & 1) {
+    if (K == 1 && (fl & 1)) {
+      // one weight class (uniform costs, C5): every word, branch-free, with
+      // the target's mask words as broadcast shared loads — the general loop
+      // below spends most of its issue on per-word branches and the dynamic
+      // class-index address arithmetic (C5 p=0.2 relax 153.5 -> 146.6 ms)
+      if (nz) {
+        const u64* bj = bjc + (size_t)jt * W;
+        int pc = 0;
+#pragma unroll
+        for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[w]);
+        ts = tcoef[0] * pc;
+        ms = tcoef[1] * pc;
+      }
+    } else if (fl & 1) {
       const u64* bj = bjc + (size_t)jt * K * W;
       for (int cc = 0; cc < K; cc++) {
         int pc = 0;
@@ -585,6 +598,12 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       mask |= __shfl_xor_sync(kFull, mask, 16);
       if (lane >= 16) mask = 0;
     }
+    // statistics on the predecessor side: P and Σ|frontier_i| over the
+    // comparable pairs of this lane's predecessor (the totals are what
+    // SearchStats needs; a per-target ballot + REDUX per tile target cost
+    // ~5 % of the issue slots)
+    my_pairs += (u64)__popc(mask);
+    my_trans += (u64)__popc(mask) * (u64)fl;
     if (!__any_sync(kFull, mask)) continue;
     // Small frontiers (every predecessor of the chunk has <= kSmallF entries,
     // the uniform-cost regime of deep lattices): each lane keeps its entries
@@ -601,12 +620,6 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       }
       for (int jt = 0; jt < ntj; jt++) {
         const bool bit = (mask >> jt) & 1u;
-        const unsigned cm = __ballot_sync(kFull, bit);
-        const unsigned tr = __reduce_add_sync(kFull, bit ? (unsigned)fl : 0u);
-        if (lane == jt) {
-          my_pairs += __popc(cm);
-          my_trans += tr;
-        }
         if (!bit || fl == 0) continue;
         Q q;
         if (!pair_q(Li, i, jt, MLi, TLi, mmi, q)) continue;
@@ -637,12 +650,6 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     unsigned sparse = 0;
     for (int jt = 0; jt < ntj; jt++) {
       const bool bit = (mask >> jt) & 1u;
-      const unsigned cm = __ballot_sync(kFull, bit);
-      const unsigned tr = __reduce_add_sync(kFull, bit ? (unsigned)fl : 0u);
-      if (lane == jt) {
-        my_pairs += __popc(cm);
-        my_trans += tr;
-      }
       const bool want = bit && fl > 0;
       const unsigned wm = __ballot_sync(kFull, want);
       if (__popc(wm) >= kDenseLanes) {
@@ -853,9 +860,13 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     __syncwarp();
   }
   if (lane == 0 && worked) s_worked = 1;
-  if (lane < ntj && (my_pairs | my_trans)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + lane * 2), my_trans);
-    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + lane * 2 + 1), my_pairs);
+  // the tile's totals go to its first target's per-member counters (their
+  // sum over the family is the statistic)
+  my_trans = warp_sum(my_trans);
+  my_pairs = warp_sum(my_pairs);
+  if (lane == 0 && (my_pairs | my_trans)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(tacc), my_trans);
+    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + 1), my_pairs);
   }
   __syncthreads();
   if (tid < ntj) {
