@@ -127,6 +127,7 @@ struct TileArgs {
                     // through the levels independently (k_solve_small)
   int qlanes;       // lanes per warp with a pair-record region (>= cw; 32 up to 8 targets)
   int off_tL, off_tB, off_tc, off_tcls, off_bjc, off_coef, off_tacc, off_pairs, off_q, off_qs, off_rows;
+  int off_tC;       // [W] intersection of the tile's target sets
   int bytes;
 };
 
@@ -147,6 +148,7 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   };
   a.off_tL = take(TJ * W * 8);
   a.off_tB = take(TJ * W * 8);
+  a.off_tC = take(W * 8);
   a.off_tc = take(TJ * 4 * 8);
   a.off_tcls = take(TJ * 8);  // per target: path flags, nonzero-word mask
   a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
@@ -373,6 +375,11 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
   if (srow)
     for (int t = tid; t < ntj * R; t += kThreads) rows[t] = INF;
   __syncthreads();
+  if (tid < W) {  // ∩ of the tile's targets: a predecessor inside it precedes all of them
+    u64 c = ~0ull;
+    for (int jt = 0; jt < ntj; jt++) c &= tL[jt * W + tid];
+    reinterpret_cast<u64*>(sm + ta.off_tC)[tid] = c;
+  }
   const int K = cv.K;
   // The pair terms need T and M of L_i ∩ ∂L_j, i.e. T(L_i) − T(L_i ∩ I_j)
   // with I_j = L_j \ ∂L_j the interior.  Wide sets (W >= 4) take, per
@@ -572,9 +579,23 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     int fl = 0;
     long long MLi = 0, TLi = 0, mmi = 0, foffi = 0;
     unsigned mask = 0;
-    if (pl < cw && i < pred_end) {
+    const bool live = pl < cw && i < pred_end;
 #pragma unroll
-      for (int w = 0; w < W; w++) Li[w] = __ldg(fv.masks + (size_t)w * F + i);
+    for (int w = 0; w < W; w++) Li[w] = live ? __ldg(fv.masks + (size_t)w * F + i) : 0ull;
+    // wide sets (deep lattices, C5: nearly every lower predecessor precedes
+    // every target): one test against the tile's intersection replaces the
+    // per-target tests when it holds for the whole warp (throughput launches
+    // only: on the narrow levels of the persistent kernel the extra vote sits
+    // on the latency path, C5 p=0.3 +3 %)
+    bool allc = false;
+    if constexpr (W >= 4 && !COH) {
+      const u64* tC = reinterpret_cast<const u64*>(sm + ta.off_tC);
+      u64 a = 0;
+#pragma unroll
+      for (int w = 0; w < W; w++) a |= Li[w] & ~tC[w];
+      allc = __all_sync(kFull, a == 0);
+    }
+    if (live) {
       if (lane == pl) {
         fl = COH ? __ldcg(flen_b + i) : flen_b[i];
         mmi = COH ? __ldcg(mmin_b + i) : mmin_b[i];
@@ -584,15 +605,16 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       }
       const int j0t = split && lane >= 16 ? 8 : 0;
       const int j1t = split && lane < 16 ? 8 : ntj;
-      for (int jt = j0t; jt < j1t; jt++) {
-        u64 acc = 0;
+      if (allc) {
+        mask = ((j1t >= 32 ? 0u : 1u << j1t) - 1u) & ~((1u << j0t) - 1u);
+      } else {
+        for (int jt = j0t; jt < j1t; jt++) {
+          u64 acc = 0;
 #pragma unroll
-        for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
-        mask |= (acc == 0 ? 1u : 0u) << jt;
+          for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
+          mask |= (acc == 0 ? 1u : 0u) << jt;
+        }
       }
-    } else {
-#pragma unroll
-      for (int w = 0; w < W; w++) Li[w] = 0;
     }
     if (split) {
       mask |= __shfl_xor_sync(kFull, mask, 16);
