@@ -18,7 +18,10 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 // resident CTAs of the wide-bitset relaxation kernel (register cap 64; a
 // 16-byte spill at W = 9; 3 CTAs at 80 registers measured 1 % slower)
-constexpr int kTile3MinBlocks = 4;
+#ifndef REMAT_TILE3_BLOCKS
+#define REMAT_TILE3_BLOCKS 4
+#endif
+constexpr int kTile3MinBlocks = REMAT_TILE3_BLOCKS;
 constexpr int kMaxTJ = 32;   // targets per tile at most (one comparable bit each)
 constexpr int kTileTJ = 8;   // targets per tile by default (REMAT_TILE_TJ)
 constexpr int kRecPerWarp = 256;  // pair-record slots per warp: lanes with records x TJ
