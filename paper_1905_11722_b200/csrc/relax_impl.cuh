@@ -22,6 +22,10 @@ constexpr int kWarps = kThreads / 32;
 #define REMAT_TILE3_BLOCKS 4
 #endif
 constexpr int kTile3MinBlocks = REMAT_TILE3_BLOCKS;
+// per-target mask rows in shared memory: wide odd widths padded to an even
+// word count, so a row is read with 16-byte loads (two words per LDS.128)
+template <int W>
+__host__ __device__ constexpr int mask_stride() { return W >= 4 ? (W + 1) & ~1 : W; }
 constexpr int kMaxTJ = 32;   // targets per tile at most (one comparable bit each)
 constexpr int kTileTJ = 8;   // targets per tile by default (REMAT_TILE_TJ)
 constexpr int kRecPerWarp = 256;  // pair-record slots per warp: lanes with records x TJ
@@ -149,12 +153,13 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
     o += (bytes + 15) & ~15;
     return at;
   };
-  a.off_tL = take(TJ * W * 8);
-  a.off_tB = take(TJ * W * 8);
+  constexpr int WS = mask_stride<W>();
+  a.off_tL = take(TJ * WS * 8);
+  a.off_tB = take(TJ * WS * 8);
   a.off_tC = take(W * 8);
   a.off_tc = take(TJ * 4 * 8);
   a.off_tcls = take(TJ * 8);  // per target: path flags, nonzero-word mask
-  a.off_bjc = take(cls ? TJ * K * W * 8 : 0);
+  a.off_bjc = take(cls ? TJ * K * WS * 8 : 0);
   a.off_coef = take(cls ? 2 * K * 8 : 0);
   a.off_tacc = take(TJ * 2 * 8);
   a.off_pairs = take(kWarps * a.qlanes * TJ * 2);
@@ -361,10 +366,11 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
   Key* rows = reinterpret_cast<Key*>(sm + ta.off_rows);
   const bool srow = ta.smem_rows;
   if (tid == 0) s_relax_worked = 0;
-  for (int e = tid; e < ntj * W; e += kThreads) {
-    const int jt = e / W, w = e - jt * W;
-    tL[e] = fv.masks[(size_t)w * F + j0 + jt];
-    tB[e] = fv.bound[(size_t)w * F + j0 + jt];
+  constexpr int WS = mask_stride<W>();
+  for (int e = tid; e < ntj * WS; e += kThreads) {
+    const int jt = e / WS, w = e - jt * WS;
+    tL[e] = w < W ? fv.masks[(size_t)w * F + j0 + jt] : 0ull;
+    tB[e] = w < W ? fv.bound[(size_t)w * F + j0 + jt] : 0ull;
   }
   for (int jt = tid; jt < ntj; jt += kThreads) {
     const long long j = j0 + jt;
@@ -380,7 +386,7 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
   __syncthreads();
   if (tid < W) {  // ∩ of the tile's targets: a predecessor inside it precedes all of them
     u64 c = ~0ull;
-    for (int jt = 0; jt < ntj; jt++) c &= tL[jt * W + tid];
+    for (int jt = 0; jt < ntj; jt++) c &= tL[jt * WS + tid];
     reinterpret_cast<u64*>(sm + ta.off_tC)[tid] = c;
   }
   const int K = cv.K;
@@ -397,7 +403,7 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
       int bc = 0, ic = 0;
       unsigned bnz = 0, inz = 0;
       for (int w = 0; w < W; w++) {
-        const u64 bw = tB[jt * W + w], iw = tL[jt * W + w] & ~bw;
+        const u64 bw = tB[jt * WS + w], iw = tL[jt * WS + w] & ~bw;
         bc += __popcll(bw);
         ic += __popcll(iw);
         bnz |= (bw != 0 ? 1u : 0u) << w;
@@ -411,23 +417,23 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
       const int bits = interior ? ic : bc;
       const unsigned nz = interior ? inz : bnz;
       if (interior)
-        for (int w = 0; w < W; w++) tB[jt * W + w] = tL[jt * W + w] & ~tB[jt * W + w];
+        for (int w = 0; w < W; w++) tB[jt * WS + w] = tL[jt * WS + w] & ~tB[jt * WS + w];
       tcls[2 * jt] = (ta.cls && 4 * K * __popc(nz) < 6 * bits ? 1 : 0) | (interior ? 2 : 0);
       tcls[2 * jt + 1] = (int)nz;
     }
     __syncthreads();
   }
   if (ta.cls) {
-    for (int e = tid; e < ntj * K * W; e += kThreads) {
-      const int jt = e / (K * W), r = e - jt * K * W, c = r / W, w = r - c * W;
-      bjc[e] = tB[jt * W + w] & cv.cls[c * W + w];
+    for (int e = tid; e < ntj * K * WS; e += kThreads) {
+      const int jt = e / (K * WS), r = e - jt * K * WS, c = r / WS, w = r - c * WS;
+      bjc[e] = w < W ? tB[jt * WS + w] & cv.cls[c * W + w] : 0ull;
     }
     for (int e = tid; e < 2 * K; e += kThreads) tcoef[e] = cv.coef[e];
   }
   if constexpr (W < 4) {
     for (int jt = tid; jt < ntj; jt += kThreads) {
       int bc = 0;
-      for (int w = 0; w < W; w++) bc += __popcll(tB[jt * W + w]);
+      for (int w = 0; w < W; w++) bc += __popcll(tB[jt * WS + w]);
       tcls[2 * jt] = ta.cls && K * W < bc;
       tcls[2 * jt + 1] = (1 << W) - 1;
     }
@@ -450,6 +456,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = (1u << lane) - 1;
   const int TJ = ta.TJ, R = ta.R, splits = ta.splits;
+  constexpr int WS = mask_stride<W>();
   const long long F = fv.F;
   const int tile = vbx / splits;
   const long long j0 = ta.jbase + (long long)tile * TJ;
@@ -510,20 +517,24 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       // below spends most of its issue on per-word branches and the dynamic
       // class-index address arithmetic (C5 p=0.2 relax 153.5 -> 146.6 ms)
       if (nz) {
-        const u64* bj = bjc + (size_t)jt * W;
+        const ulonglong2* bj2 = reinterpret_cast<const ulonglong2*>(bjc + (size_t)jt * WS);
         int pc = 0;
 #pragma unroll
-        for (int w = 0; w < W; w++) pc += __popcll(Li[w] & bj[w]);
+        for (int w = 0; w < W; w += 2) {
+          const ulonglong2 b = bj2[w / 2];  // one LDS.128 (padding word is 0)
+          pc += __popcll(Li[w] & b.x);
+          if (w + 1 < W) pc += __popcll(Li[w + 1] & b.y);
+        }
         ts = tcoef[0] * pc;
         ms = tcoef[1] * pc;
       }
     } else if (fl & 1) {
-      const u64* bj = bjc + (size_t)jt * K * W;
+      const u64* bj = bjc + (size_t)jt * K * WS;
       for (int cc = 0; cc < K; cc++) {
         int pc = 0;
 #pragma unroll
         for (int w = 0; w < W; w++)
-          if (W < 4 || ((nz >> w) & 1u)) pc += __popcll(Li[w] & bj[cc * W + w]);
+          if (W < 4 || ((nz >> w) & 1u)) pc += __popcll(Li[w] & bj[cc * WS + w]);
         ts += tcoef[2 * cc] * pc;
         ms += tcoef[2 * cc + 1] * pc;
       }
@@ -531,7 +542,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
 #pragma unroll
       for (int w = 0; w < W; w++) {
         if (W >= 4 && !((nz >> w) & 1u)) continue;
-        u64 x = Li[w] & tB[jt * W + w];
+        u64 x = Li[w] & tB[jt * WS + w];
         while (x) {
           const int v = w * 64 + __ffsll((long long)x) - 1;
           x &= x - 1;
@@ -613,8 +624,18 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       } else {
         for (int jt = j0t; jt < j1t; jt++) {
           u64 acc = 0;
+          if constexpr (WS > W || (W >= 4 && W % 2 == 0)) {
+            const ulonglong2* t2 = reinterpret_cast<const ulonglong2*>(tL + jt * WS);
 #pragma unroll
-          for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
+            for (int w = 0; w < W; w += 2) {
+              const ulonglong2 t = t2[w / 2];
+              acc |= Li[w] & ~t.x;
+              if (w + 1 < W) acc |= Li[w + 1] & ~t.y;
+            }
+          } else {
+#pragma unroll
+            for (int w = 0; w < W; w++) acc |= Li[w] & ~tL[jt * W + w];
+          }
           mask |= (acc == 0 ? 1u : 0u) << jt;
         }
       }
