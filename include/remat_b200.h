@@ -103,8 +103,10 @@ REMAT_API int remat_family_free(remat_family_t f);
 REMAT_API int remat_family_timings(remat_family_t f, remat_timings *out);
 /* Per-member figures of the last solve's budget `b` for members
  * [start, start+count): |frontier| (SearchStats.states_visited terms), |cell|
- * (table_entries terms), Σ|frontier_i| over comparable predecessors
- * (transitions terms, planner.py:164) and the comparable-predecessor count.
+ * (table_entries terms), and the transitions (planner.py:164) and
+ * comparable-pair counts of the member's LEVEL, accumulated per relaxation
+ * tile on the tile's first target (their sum over any run of whole levels is
+ * exact; the dense relaxation no longer attributes them per target).
  * Any output may be NULL.  Diagnostics for the per-level work profile. */
 REMAT_API int remat_family_member_stats(remat_family_t f, int32_t b, int64_t start,
                                         int64_t count, int32_t *flen, int32_t *cells,

@@ -409,8 +409,10 @@ class DeviceFamily:
         return array_to_masks(buf[:count])
 
     def member_stats(self, b: int = 0) -> dict:
-        """Per-member |frontier|, |cell|, Σ|frontier_i| and comparable-pair
-        count of the last solve's budget ``b`` (numpy arrays of length F)."""
+        """Per-member |frontier| and |cell| of the last solve's budget ``b``,
+        plus transitions and comparable-pair counts accumulated per relaxation
+        tile on the tile's first target (sums over whole levels are exact;
+        numpy arrays of length F)."""
         F = self.size
         out = {"flen": np.zeros(F, np.int32), "cells": np.zeros(F, np.int32),
                "trans": np.zeros(F, np.uint64), "pairs": np.zeros(F, np.uint64)}
