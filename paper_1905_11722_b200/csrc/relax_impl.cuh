@@ -144,7 +144,11 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   TileArgs a{};
   a.TJ = TJ;
   a.R = R;
-  a.qlanes = std::max(1, std::min(32, kRecPerWarp / TJ));
+  static const int rec_env = [] {  // REMAT_REC_PER_WARP: record slots per warp (A/B)
+    const char* e = getenv("REMAT_REC_PER_WARP");
+    return e ? std::max(32, atoi(e)) : kRecPerWarp;
+  }();
+  a.qlanes = std::max(1, std::min(32, rec_env / TJ));
   a.smem_rows = smem_rows;
   a.cls = cls;
   int o = 0;
@@ -1365,7 +1369,11 @@ int plan_level_w(remat_family_s* f, int lvl, long long lo, long long hi, TileArg
   // more than two more rows (PSPNet full sweep, rows of 1.4 k slots: 8 -> 6
   // targets kept a third CTA per SM resident, -9 %)
   if (!single_cta) {
-    const int occ = W >= 4 ? kTile3MinBlocks : 4;
+    static const int occ_env = [] {  // REMAT_TILE_OCC: resident-CTA target (A/B)
+      const char* e = getenv("REMAT_TILE_OCC");
+      return e ? std::max(1, atoi(e)) : 0;
+    }();
+    const int occ = occ_env ? occ_env : (W >= 4 ? kTile3MinBlocks : 4);
     const int per_cta = (228 << 10) / occ - (1 << 10);
     while (TJ > 1 && ta.bytes > per_cta) {
       --TJ;
