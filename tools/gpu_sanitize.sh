@@ -28,8 +28,18 @@ s.close()
 os.environ["REMAT_SHARD_REPLICATE"] = "0"
 print(loopback_plans(g, [2 * g.total_memory], 2)[0].objective_value)
 del os.environ["REMAT_SHARD_REPLICATE"]
-import json
+# round 2 (late): wide bitsets (W = 5) through the per-level tile kernel:
+# tile-intersection subset test, one-class pair terms over padded 16-byte rows
+import random
 from paper_1905_11722_b200.graph import graph_from_document
+rng = random.Random(3)
+doc = {"nodes": [{"id": f"r{i}", "compute_cost": 3, "memory_cost": 5} for i in range(300)],
+       "edges": [[f"r{i}", f"r{j}"] for i in range(300) for j in range(i + 1, 300) if rng.random() < 0.33]}
+g3 = graph_from_document(doc)
+s = Solver(g3, "full", 30_000)
+print("wide", s.size if hasattr(s, "size") else "", [p.objective_value for p in s.plans([2 * g3.total_memory, g3.total_memory])])
+s.close()
+import json
 rec = json.load(open("tests/golden/large_costs.json"))["data"][5]
 g2 = graph_from_document(rec["graph"])
 print(dp_plan(PlanRequest(g2, 2 * g2.total_memory, "full")).objective_value)
