@@ -77,10 +77,10 @@ struct Traits<true> {
   static constexpr unsigned INF = 0xffffffffu;
   // one LDG.64 per entry (entries of earlier levels are read-only while a
   // level is relaxed, so the non-coherent path is safe)
-  template <bool COH = false>
+  template <int MODE = 0>
   static __device__ __forceinline__ void load(const E* p, unsigned& t, unsigned& m) {
     const uint2* q = reinterpret_cast<const uint2*>(p);
-    const uint2 v = COH ? __ldcg(q) : __ldg(q);
+    const uint2 v = MODE == 1 ? __ldcg(q) : MODE == 2 ? __ldca(q) : __ldg(q);
     t = v.x;
     m = v.y;
   }
@@ -104,15 +104,28 @@ struct Traits<false> {
   using Q = PairQW;
   using M = long long;
   static constexpr u64 INF = ~0ull;
-  template <bool COH = false>
+  template <int MODE = 0>
   static __device__ __forceinline__ void load(const E* p, unsigned& t, long long& m) {
     const longlong2* q = reinterpret_cast<const longlong2*>(p);
-    const longlong2 v = COH ? __ldcg(q) : __ldg(q);
+    const longlong2 v = MODE == 1 ? __ldcg(q) : MODE == 2 ? __ldca(q) : __ldg(q);
     t = (unsigned)v.x;
     m = v.y;
   }
   static __device__ __forceinline__ PairQW lds(const PairQW* p) { return *p; }
 };
+
+// Loads of the DP table being built (frontier entries, |frontier|, smallest m):
+//   0  non-coherent path (per-level launches: the table is read-only here)
+//   1  L2 only, ld.cg (persistent multi-level kernel: other SMs wrote it)
+//   2  L1-cacheable, ld.ca (one CTA per budget walks every level and reads
+//      only what it wrote itself, ordered by __syncthreads; chain-like
+//      lattices read each predecessor at every later level, so it stays in L1)
+template <int MODE, typename T>
+__device__ __forceinline__ T ld_dp(const T* p) {
+  if constexpr (MODE == 1) return __ldcg(p);
+  else if constexpr (MODE == 2) return __ldca(p);
+  else return *p;
+}
 
 // Shared-memory carve-up of k_relax_tile (host and device agree on it).
 struct TileArgs {
@@ -445,7 +458,8 @@ __device__ __forceinline__ void tile_setup(const FamilyView& fv, const ClassView
   __syncthreads();
 }
 
-template <int W, bool NARROW, bool COH, bool DUAL = false>
+template <int W, bool NARROW, bool COH, bool DUAL = false,
+          int LDM = !COH ? 0 : (DUAL ? 2 : 1)>
 __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView& g,
                                            const ClassView& cv, const DpView& dp,
                                            const TileArgs& ta, const int vbx, const int b,
@@ -615,8 +629,8 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
     }
     if (live) {
       if (lane == pl) {
-        fl = COH ? __ldcg(flen_b + i) : flen_b[i];
-        mmi = COH ? __ldcg(mmin_b + i) : mmin_b[i];
+        fl = ld_dp<LDM>(flen_b + i);
+        mmi = ld_dp<LDM>(mmin_b + i);
         MLi = __ldg(fv.ML + i);
         TLi = __ldg(fv.TL + i);
         foffi = __ldg(fv.foff + i);
@@ -666,7 +680,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
       for (int e = 0; e < kSmallF; e++) {
         et[e] = 0;
         em[e] = 0;
-        if (e < fl) Traits<NARROW>::template load<COH>(fe + (fbase + foffi + e), et[e], em[e]);
+        if (e < fl) Traits<NARROW>::template load<LDM>(fe + (fbase + foffi + e), et[e], em[e]);
       }
       for (int jt = 0; jt < ntj; jt++) {
         const bool bit = (mask >> jt) & 1u;
@@ -747,7 +761,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         for (int w = 0; w < W; w++) Lp[w] = __ldg(fv.masks + (size_t)w * F + ii);
         Q q;
         if (pair_q(Lp, ii, jt, __ldg(fv.ML + ii), __ldg(fv.TL + ii),
-                   COH ? __ldcg(mmin_b + ii) : mmin_b[ii], q))
+                   ld_dp<LDM>(mmin_b + ii), q))
           wq[pl * TJ + atomicAdd(wpc + pl, 1)] = q;
       }
     }
@@ -796,7 +810,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         v = lane < tot;
         if (v) {
           rec = ld_rec(wrec + k);
-          Traits<NARROW>::template load<COH>(static_cast<const E*>(rec.ptr) + lane, t, m);
+          Traits<NARROW>::template load<LDM>(static_cast<const E*>(rec.ptr) + lane, t, m);
         }
       }
       for (int r = 0; r < tot; r += 32) {
@@ -809,7 +823,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
           vn = r + 32 + lane < tot;
           if (vn) {
             recn = ld_rec(wrec + kn);
-            Traits<NARROW>::template load<COH>(static_cast<const E*>(recn.ptr) + (r + 32 + lane), tn, mn);
+            Traits<NARROW>::template load<LDM>(static_cast<const E*>(recn.ptr) + (r + 32 + lane), tn, mn);
           }
         }
         if (v) {
@@ -866,11 +880,11 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
         x1.v = e0 + 1 < tot;
         if (x0.v) {
           x0.rec = wrec[k0];
-          Traits<NARROW>::template load<COH>(static_cast<const E*>(x0.rec.ptr) + e0, x0.t, x0.m);
+          Traits<NARROW>::template load<LDM>(static_cast<const E*>(x0.rec.ptr) + e0, x0.t, x0.m);
         }
         if (x1.v) {
           x1.rec = wrec[k1];
-          Traits<NARROW>::template load<COH>(static_cast<const E*>(x1.rec.ptr) + (e0 + 1), x1.t, x1.m);
+          Traits<NARROW>::template load<LDM>(static_cast<const E*>(x1.rec.ptr) + (e0 + 1), x1.t, x1.m);
         }
       };
       auto relax = [&](const Item& x) {
@@ -1029,9 +1043,8 @@ __global__ void __launch_bounds__(kThreads)
       relax_body<W, NARROW, true, true>(fv, g, cv, dp, ta, t, b, nb, sm);
       __syncthreads();
     }
-    // the next level reads this one through L2 (ld.cg): make the finalized
-    // frontier entries and records visible there before any warp proceeds
-    __threadfence();
+    // the next level reads this one (ld.ca, relax_body LDM 2): the CTA
+    // barrier orders the finalized entries and records for every warp
     __syncthreads();
   }
 }
