@@ -352,6 +352,78 @@ __device__ void finalize_row_warp(const typename Traits<NARROW>::Key* row, int R
   }
 }
 
+// K5 for a tile of ONE target (chain-like levels: C1, C3, narrow C5 levels)
+// with the whole CTA: each thread scans Rj/256 slots, block scans give the
+// prefix-min and the output positions — instead of one warp walking the row
+// three times while seven wait at the next barrier (k_solve_small: barrier
+// stalls 8.6 per issued instruction on C3).  Called by every thread.
+// `scr`: >= 36 u64 of dynamic shared memory free at finalize time (the
+// tile's pair-record region: static shared memory here would cost the
+// per-level kernels a resident CTA).
+template <bool NARROW>
+__device__ void finalize_row_block(const typename Traits<NARROW>::Key* row, int Rj,
+                                   const DpView& dp, const FamilyView& fv, long long j, int b,
+                                   u64* scr) {
+  using Key = typename Traits<NARROW>::Key;
+  using E = typename Traits<NARROW>::E;
+  constexpr Key INF = Traits<NARROW>::INF;
+  u64* s_scr = scr;
+  u64& s_gmin = scr[35];
+  const int tid = threadIdx.x;
+  const int IB = dp.IB;
+  const bool mx = dp.maximize;
+  const int per = (Rj + kThreads - 1) / kThreads;
+  const int s0 = min(Rj, tid * per), s1 = min(Rj, s0 + per);
+  u64 lmin = ~0ull, cells = 0;
+  for (int q = s0; q < s1; q++) {
+    const Key key = row[mx ? Rj - 1 - q : q];
+    if (key != INF) {
+      cells++;
+      const u64 m = (u64)(key >> IB);
+      lmin = m < lmin ? m : lmin;
+    }
+  }
+  if (tid == 0) s_gmin = ~0ull;
+  const u64 pm = block_exclusive_min(lmin, s_scr);
+  if (lmin != ~0ull) atomicMin(reinterpret_cast<unsigned long long*>(&s_gmin), lmin);
+  u64 nf = 0, run = pm;
+  for (int q = s0; q < s1; q++) {
+    const Key key = row[mx ? Rj - 1 - q : q];
+    if (key != INF && (u64)(key >> IB) < run) {
+      nf++;
+      run = (u64)(key >> IB);
+    }
+  }
+  // one scan for both counts: |frontier| in the high half, |cell| in the low
+  u64 both_tot;
+  u64 pos = block_exclusive_sum((nf << 32) | cells, s_scr, &both_tot) >> 32;
+  const u64 nf_tot = both_tot >> 32, cells_tot = both_tot & 0xffffffffull;
+  const long long slot0 = (long long)b * dp.slots + fv.foff[j];
+  E* out = reinterpret_cast<E*>(dp.fe) + slot0;
+  int* par = dp.parent + slot0;
+  const Key pmask = (Key(1) << IB) - 1;
+  run = pm;
+  for (int q = s0; q < s1; q++) {
+    const int t = mx ? Rj - 1 - q : q;
+    const Key key = row[t];
+    if (key != INF && (u64)(key >> IB) < run) {
+      run = (u64)(key >> IB);
+      E e{};
+      e.t = (unsigned)t;
+      e.m = (decltype(e.m))run;
+      out[pos] = e;
+      par[pos] = (int)(key & pmask);
+      pos++;
+    }
+  }
+  if (tid == 0) {
+    const size_t at = (size_t)b * fv.F + j;
+    dp.flen[at] = (int)nf_tot;
+    dp.ccount[at] = (int)cells_tot;
+    dp.mmin[at] = nf_tot ? (long long)s_gmin : LLONG_MAX;
+  }
+}
+
 // K4 (+K5): one (tile, split) "virtual CTA" `vbx` of budget b.  Run either as
 // one CTA of k_relax_tile (grid (tiles·splits, nb)) or inside the persistent
 // k_relax_levels loop.
@@ -953,9 +1025,13 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   }
   unsigned* done = ctr + (size_t)nb * ta.ctr_stride;  // finished CTAs of the tile
   if (splits == 1 && srow) {
-    for (int jt = warp; jt < ntj; jt += kWarps)
-      finalize_row_warp<NARROW>(rows + jt * R, (int)(fv.TL[j0 + jt] + 1), dp,
-                                fv, j0 + jt, b);
+    if (DUAL && ntj == 1)
+      finalize_row_block<NARROW>(rows, (int)(fv.TL[j0] + 1), dp, fv, j0, b,
+                                 reinterpret_cast<u64*>(sm + ta.off_q));
+    else
+      for (int jt = warp; jt < ntj; jt += kWarps)
+        finalize_row_warp<NARROW>(rows + jt * R, (int)(fv.TL[j0 + jt] + 1), dp,
+                                  fv, j0 + jt, b);
     if (tid == 0) *ctr = 0;  // counters are self-resetting for the next level
     return;
   }
