@@ -1112,16 +1112,28 @@ __global__ void __launch_bounds__(kThreads)
     k_solve_small(FamilyView fv, GraphView g, ClassView cv, DpView dp,
                   const TileArgs* __restrict__ levels, int nlev, int nb) {
   extern __shared__ __align__(16) unsigned char sm[];
+  // level plans staged through shared memory one level ahead: the next
+  // level's arguments are fetched while this one relaxes, not on the
+  // level-to-level critical path
+  constexpr int kTaWords = (int)(sizeof(TileArgs) / 4);
+  static_assert(sizeof(TileArgs) % 4 == 0, "TileArgs is copied as 32-bit words");
+  __shared__ __align__(16) TileArgs s_ta[2];
   const int b = blockIdx.y;
+  if (nlev > 0)
+    for (int k = threadIdx.x; k < kTaWords; k += kThreads)
+      reinterpret_cast<int*>(&s_ta[0])[k] = reinterpret_cast<const int*>(&levels[0])[k];
+  __syncthreads();
   for (int l = 0; l < nlev; l++) {
-    const TileArgs ta = levels[l];
+    const TileArgs ta = s_ta[l & 1];
+    if (l + 1 < nlev)
+      for (int k = threadIdx.x; k < kTaWords; k += kThreads)
+        reinterpret_cast<int*>(&s_ta[(l + 1) & 1])[k] = reinterpret_cast<const int*>(&levels[l + 1])[k];
     for (int t = 0; t < ta.tiles; t++) {
+      // the next tile / level reads this one (ld.ca, relax_body LDM 2) and
+      // reuses its shared memory: the CTA barrier orders both
       relax_body<W, NARROW, true, true>(fv, g, cv, dp, ta, t, b, nb, sm);
       __syncthreads();
     }
-    // the next level reads this one (ld.ca, relax_body LDM 2): the CTA
-    // barrier orders the finalized entries and records for every warp
-    __syncthreads();
   }
 }
 
