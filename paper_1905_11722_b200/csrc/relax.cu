@@ -138,7 +138,11 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
   // one CTA per budget pays off when the batch itself fills the GPU and the
   // frontiers are short (maximize keeps a few entries per cell);
   // a single budget, or long minimize frontiers, spread each level over CTAs
-  const bool small_ok = objective == REMAT_MAXIMIZE ? budgets.size() >= 16 : budgets.size() >= 48;
+  // unless the batch has a CTA for every SM (C4 pruned 64-budget sweep:
+  // one CTA per budget 17.97 ms, per-level launches 16.84 ms)
+  const bool small_ok = objective == REMAT_MAXIMIZE
+                            ? budgets.size() >= 16
+                            : budgets.size() >= (size_t)sm_count(f->g->device);
   if (f->F <= small_family && small_ok) {
     if ((rc = solve_small(f)) < 0) return rc;
     if (rc == REMAT_OK) return solve_finish(f, info, chain_masks, cached_masks, stage_memory);

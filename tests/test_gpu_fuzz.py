@@ -95,3 +95,29 @@ def test_fuzz_level_sharding_loopback_against_oracle(seed):
                 for b, plan in zip(budgets, plans):
                     ref = orc.dp_plan(g, b, fam, obj, cap=5_000)
                     assert_plan_matches(plan, ref, (seed, kind, world, fam, obj, b))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_one_cta_per_budget_minimize(seed):
+    """Minimize batches with a budget for every SM and more run whole in the
+    one-CTA-per-budget solver (k_solve_small, 64-item steps over long
+    frontiers): every field equals the oracle's."""
+    from oracle import oracle as orc
+
+    rng = random.Random(9000 + seed)
+    while True:
+        g, kind = _graph(rng)
+        try:
+            F = len(orc.family(g, "full", 1_000))
+        except RuntimeError:
+            continue
+        break
+    top = 2 * g.total_memory
+    budgets = sorted([rng.randint(0, top) for _ in range(159)] + [top])  # repeats allowed
+    for fam in ("full", "pruned"):
+        s = Solver(g, fam, 1_000)
+        plans = s.plans(budgets, "minimize")
+        for b, plan in zip(budgets, plans):
+            ref = orc.dp_plan(g, b, fam, "minimize", cap=1_000)
+            assert_plan_matches(plan, ref, (seed, kind, g.n, F, fam, b))
+        s.close()
