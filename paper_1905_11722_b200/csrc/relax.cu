@@ -140,9 +140,13 @@ int solve_batch(remat_family_s* f, const std::vector<long long>& budgets, int ob
   // a single budget, or long minimize frontiers, spread each level over CTAs
   // unless the batch has a CTA for every SM (C4 pruned 64-budget sweep:
   // one CTA per budget 17.97 ms, per-level launches 16.84 ms)
-  const bool small_ok = objective == REMAT_MAXIMIZE
-                            ? budgets.size() >= 16
-                            : budgets.size() >= (size_t)sm_count(f->g->device);
+  static const int force_small = [] {  // REMAT_FORCE_SMALL=1: any batch (A/B hook)
+    const char* e = getenv("REMAT_FORCE_SMALL");
+    return e ? atoi(e) : 0;
+  }();
+  const bool small_ok = force_small || (objective == REMAT_MAXIMIZE
+                                            ? budgets.size() >= 16
+                                            : budgets.size() >= (size_t)sm_count(f->g->device));
   if (f->F <= small_family && small_ok) {
     if ((rc = solve_small(f)) < 0) return rc;
     if (rc == REMAT_OK) return solve_finish(f, info, chain_masks, cached_masks, stage_memory);
