@@ -182,21 +182,10 @@ __global__ void __launch_bounds__(kThreads)
       TLi = __ldg(fv.TL + i);
       foffi = __ldg(fv.foff + i);
     }
-    // statistics: lane jt collects target jt (comparable pairs, Σ|frontier|)
-    {
-      unsigned any = __reduce_or_sync(kFull, mask);
-      while (any) {
-        const int jt = __ffs(any) - 1;
-        any &= any - 1;
-        const bool bit = (mask >> jt) & 1u;
-        const unsigned cm = __ballot_sync(kFull, bit);
-        const unsigned tr = __reduce_add_sync(kFull, bit ? (unsigned)fl : 0u);
-        if (lane == jt) {
-          my_pairs += __popc(cm);
-          my_trans += tr;
-        }
-      }
-    }
+    // statistics on the predecessor side (comparable pairs, Σ|frontier|): the
+    // tile's totals land on its first target, as in relax_body
+    my_pairs += (u64)__popc(mask);
+    my_trans += (u64)__popc(mask) * (u64)fl;
     unsigned want = fl > 0 ? mask : 0u;
     // records, in rounds of at most kPmRecCap per warp
     while (__any_sync(kFull, want)) {
@@ -300,9 +289,11 @@ __global__ void __launch_bounds__(kThreads)
       __syncwarp();
     }
   }
-  if (lane < ntj && (my_pairs | my_trans)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + lane * 2), my_trans);
-    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + lane * 2 + 1), my_pairs);
+  my_trans = warp_sum(my_trans);
+  my_pairs = warp_sum(my_pairs);
+  if (lane == 0 && (my_pairs | my_trans)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(tacc), my_trans);
+    atomicAdd(reinterpret_cast<unsigned long long*>(tacc + 1), my_pairs);
   }
   __syncthreads();
   if (tid < ntj) {
