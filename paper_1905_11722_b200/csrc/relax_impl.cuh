@@ -179,9 +179,12 @@ static TileArgs tile_layout(int TJ, int R, int K, bool smem_rows, bool cls) {
   a.off_bjc = take(cls ? TJ * K * WS * 8 : 0);
   a.off_coef = take(cls ? 2 * K * 8 : 0);
   a.off_tacc = take(TJ * 2 * 8);
-  a.off_pairs = take(kWarps * a.qlanes * TJ * 2);
   a.off_q = take(kWarps * a.qlanes * TJ * (int)sizeof(typename Traits<NARROW>::Q));
   a.off_qs = take(kWarps * 32 * (16 + 4));
+  // a warp's sparse-pair list (<= qlanes·TJ <= 256 u16) lives in its live-
+  // predecessor slots (32 x 16 B): the list is consumed before those are
+  // written, and the 4 KB saved buys a wider tile at 4 CTAs per SM
+  a.off_pairs = a.off_qs;
   a.off_rows = take(smem_rows ? TJ * R * (int)sizeof(Key) : 0);
   a.bytes = o;
   return a;
@@ -560,7 +563,7 @@ __device__ __forceinline__ void relax_body(const FamilyView& fv, const GraphView
   long long* tcoef = reinterpret_cast<long long*>(sm + ta.off_coef);  // [K][2]
   u64* tacc = reinterpret_cast<u64*>(sm + ta.off_tacc);     // [TJ][2]
   unsigned short* wpairs =
-      reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * ta.qlanes * TJ;
+      reinterpret_cast<unsigned short*>(sm + ta.off_pairs) + warp * 256;  // aliases wrec
   Q* wq = reinterpret_cast<Q*>(sm + ta.off_q) + warp * ta.qlanes * TJ;  // feasible pairs of a chunk
   const unsigned wq_sa = (unsigned)__cvta_generic_to_shared(wq);
   PredRec* wrec = reinterpret_cast<PredRec*>(sm + ta.off_qs) + warp * 32;  // live predecessors
