@@ -19,3 +19,16 @@ for seed in range(a, b):
 for seed in range(a, a + (b - a) // 4):
     m.test_fuzz_level_sharding_loopback_against_oracle(seed)
 print("all ok", b - a, "seeds", round(time.time() - t0, 1))
+# wide bitsets (tests/test_gpu_wide.py) and the one-CTA-per-budget minimize
+# solver, seeds beyond the suite's: FUZZ_WIDE=<count>
+import os  # noqa: E402
+
+nw = int(os.environ.get("FUZZ_WIDE", "0"))
+if nw:
+    spec2 = importlib.util.spec_from_file_location("wd", ROOT / "tests" / "test_gpu_wide.py")
+    wd = importlib.util.module_from_spec(spec2)
+    spec2.loader.exec_module(wd)
+    for seed in range(a, a + nw):
+        wd.test_wide_dense_dags_against_oracle(seed)
+        m.test_fuzz_one_cta_per_budget_minimize(seed)
+    print("wide + one-CTA minimize ok", nw, "seeds", round(time.time() - t0, 1))
